@@ -1,0 +1,227 @@
+"""CPU oracle for the executor's forward: numpy restatement of every b200-plan op.
+
+TEST INFRASTRUCTURE ONLY.  Imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs — never by the product path
+(paper_2006_05096_b200/ must fail loudly without libb2.so instead of falling
+back here).
+
+What it restates.  The reference executor, MockServer.predict
+(pkg/src/modelci/mockserve/server.py:117-127), returns zeros after a sleep and
+computes nothing, so there is no reference forward to follow line by line.
+The forward semantics are the ones the converter defines (zoo.py docstring,
+plan.py op table), and this oracle follows them op by op in
+float64 (or float32).  It is pinned two ways (tests/test_oracle.py):
+
+* toy graphs (C1): against oracle/toyref.c, an independent C fp64 restatement
+  of the toy op semantics over the reference's toy-binary layout
+  (toyformat.py:117-149), and against tests/golden/mlp_golden.json;
+* torchvision ResNet-50 / MobileNetV2 / VGG-16 and transformers BertModel
+  (third-party modules absent from /root/reference; versions torchvision
+  0.26.0, transformers 5.5.0 as installed in this image): against the modules'
+  own fp64 CPU forward at small batch (tests/test_oracle.py, CPU only).
+
+Weights are the plan's fp32 values (BN already folded by the converter).
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2006_05096_b200 import plan as P  # noqa: E402
+
+try:
+    from scipy.special import erf as _erf
+except ImportError:  # pragma: no cover
+    _erf = np.vectorize(math.erf)
+
+
+def _act(x, code):
+    if code == P.ACT_NONE:
+        return x
+    if code == P.ACT_RELU:
+        return np.maximum(x, 0)
+    if code == P.ACT_RELU6:
+        return np.clip(x, 0, 6)
+    if code == P.ACT_GELU:
+        return 0.5 * x * (1.0 + _erf(x / math.sqrt(2.0)))
+    if code == P.ACT_TANH:
+        return np.tanh(x)
+    raise ValueError(f"unknown activation {code}")
+
+
+def _pad_hw(x, pad, value=0.0):
+    if pad == 0:
+        return x
+    return np.pad(x, ((0, 0), (pad, pad), (pad, pad), (0, 0)), constant_values=value)
+
+
+def conv2d_nhwc(x, w, bias, stride, pad):
+    """x [B,H,W,C], w [Cout,R,S,C] -> [B,OH,OW,Cout] via im2col + GEMM."""
+    B, H, W, C = x.shape
+    cout, R, S, _ = w.shape
+    xp = _pad_hw(x, pad)
+    OH = (H + 2 * pad - R) // stride + 1
+    OW = (W + 2 * pad - S) // stride + 1
+    sb, sh, sw, sc = xp.strides
+    cols = np.lib.stride_tricks.as_strided(
+        xp, shape=(B, OH, OW, R, S, C), strides=(sb, sh * stride, sw * stride, sh, sw, sc))
+    out = cols.reshape(B * OH * OW, R * S * C) @ w.reshape(cout, R * S * C).T
+    if bias is not None:
+        out = out + bias
+    return out.reshape(B, OH, OW, cout)
+
+
+def dwconv_nhwc(x, w, bias, stride, pad):
+    B, H, W, C = x.shape
+    R = w.shape[1]
+    xp = _pad_hw(x, pad)
+    OH = (H + 2 * pad - R) // stride + 1
+    OW = (W + 2 * pad - R) // stride + 1
+    out = np.zeros((B, OH, OW, C), dtype=x.dtype)
+    for r in range(R):
+        for s in range(R):
+            out += xp[:, r:r + stride * OH:stride, s:s + stride * OW:stride, :] * w[:, r, s]
+    if bias is not None:
+        out += bias
+    return out
+
+
+def maxpool_nhwc(x, k, stride, pad):
+    B, H, W, C = x.shape
+    xp = _pad_hw(x, pad, -np.inf)
+    OH = (H + 2 * pad - k) // stride + 1
+    OW = (W + 2 * pad - k) // stride + 1
+    out = np.full((B, OH, OW, C), -np.inf, dtype=x.dtype)
+    for r in range(k):
+        for s in range(k):
+            np.maximum(out, xp[:, r:r + stride * OH:stride, s:s + stride * OW:stride, :], out=out)
+    return out
+
+
+def layernorm(x, g, b, eps):
+    mu = x.mean(-1, keepdims=True)
+    var = ((x - mu) ** 2).mean(-1, keepdims=True)
+    return (x - mu) / np.sqrt(var + eps) * g + b
+
+
+def attention(qkv, heads, dh):
+    """qkv [B,S,3*H*Dh] -> [B,S,H*Dh]; softmax(QK^T/sqrt(Dh)) V, no mask."""
+    B, S, _ = qkv.shape
+    q, k, v = np.split(qkv.reshape(B, S, 3, heads, dh), 3, axis=2)
+    q, k, v = (t[:, :, 0].transpose(0, 2, 1, 3) for t in (q, k, v))   # [B,H,S,Dh]
+    sc = q @ k.transpose(0, 1, 3, 2) / math.sqrt(dh)
+    sc = sc - sc.max(-1, keepdims=True)
+    p = np.exp(sc)
+    p /= p.sum(-1, keepdims=True)
+    return (p @ v).transpose(0, 2, 1, 3).reshape(B, S, heads * dh)
+
+
+def forward(plan, x, dtype=np.float64):
+    """Run a decoded plan (plan.decode) on a host batch.
+
+    ``x``: dense inputs [B, in_elems] (float) or token ids [B, seq] (int).
+    Returns the fp output [B, out_elems] in ``dtype``.
+    """
+    if isinstance(plan, (bytes, bytearray)):
+        plan = P.decode(plan)
+    W = [w.astype(dtype) for w in plan.weights]
+    B = x.shape[0]
+    T: dict[int, np.ndarray] = {}
+
+    def shaped(t):
+        return T[t].reshape((B,) + plan.tensors[t].shape)
+
+    def wt(i):
+        return None if i < 0 else W[i]
+
+    out = np.zeros((B, plan.out_elems), dtype=dtype)
+    for o in plan.ops:
+        k = o.kind
+        if k == P.OP_INPUT:
+            C, H, Wd, Cp = o[P.P_IN_C], o[P.P_IN_H], o[P.P_IN_W], o[P.P_IN_CPAD]
+            img = np.asarray(x, dtype=dtype).reshape(B, C, H, Wd).transpose(0, 2, 3, 1)
+            buf = np.zeros((B, H, Wd, Cp), dtype=dtype)
+            buf[..., :C] = img
+            T[o[P.P_IN_OUT]] = buf
+        elif k == P.OP_TOKENS:
+            T[o[P.P_TK_OUT]] = np.asarray(x, dtype=np.int64).reshape(B, o[P.P_TK_SEQ])
+        elif k == P.OP_CONV:
+            y = conv2d_nhwc(shaped(o[P.P_CV_IN]), W[o[P.P_CV_W]], wt(o[P.P_CV_B]),
+                            o[P.P_CV_STRIDE], o[P.P_CV_PAD])
+            if o[P.P_CV_RES] >= 0:
+                y = y + shaped(o[P.P_CV_RES])
+            T[o[P.P_CV_OUT]] = _act(y, o[P.P_CV_ACT])
+        elif k == P.OP_LINEAR:
+            K, N, rows, astride = o[P.P_LN_K], o[P.P_LN_N], o[P.P_LN_ROWS], o[P.P_LN_ASTRIDE]
+            flat = T[o[P.P_LN_IN]].reshape(B, -1)
+            idx = np.arange(rows)[:, None] * astride + np.arange(K)[None, :]
+            a = flat[:, idx]                                     # [B, rows, K]
+            y = a @ W[o[P.P_LN_W]].T
+            if o[P.P_LN_B] >= 0:
+                y = y + W[o[P.P_LN_B]]
+            if o[P.P_LN_RES] >= 0:
+                y = y + T[o[P.P_LN_RES]].reshape(B, rows, N)
+            T[o[P.P_LN_OUT]] = _act(y, o[P.P_LN_ACT])
+        elif k == P.OP_DWCONV:
+            y = dwconv_nhwc(shaped(o[P.P_DW_IN]), W[o[P.P_DW_W]], wt(o[P.P_DW_B]),
+                            o[P.P_DW_STRIDE], o[P.P_DW_PAD])
+            T[o[P.P_DW_OUT]] = _act(y, o[P.P_DW_ACT])
+        elif k == P.OP_MAXPOOL:
+            T[o[P.P_MP_OUT]] = maxpool_nhwc(shaped(o[P.P_MP_IN]), o[P.P_MP_K],
+                                            o[P.P_MP_STRIDE], o[P.P_MP_PAD])
+        elif k == P.OP_AVGPOOL:
+            T[o[P.P_AP_OUT]] = shaped(o[P.P_AP_IN]).mean(axis=(1, 2))
+        elif k == P.OP_LAYERNORM:
+            D, rows = o[P.P_LNM_D], o[P.P_LNM_ROWS]
+            v = T[o[P.P_LNM_IN]].reshape(B, rows, D)
+            if o[P.P_LNM_RES] >= 0:
+                v = v + T[o[P.P_LNM_RES]].reshape(B, rows, D)
+            T[o[P.P_LNM_OUT]] = layernorm(v, W[o[P.P_LNM_G]], W[o[P.P_LNM_B]],
+                                          P.bits_f32(o[P.P_LNM_EPS]))
+        elif k == P.OP_EMBED:
+            ids = T[o[P.P_EM_IDS]]
+            e = W[o[P.P_EM_WORD]][ids] + W[o[P.P_EM_POS]][None, :ids.shape[1]] + \
+                W[o[P.P_EM_TYPE]][None, None, :]
+            T[o[P.P_EM_OUT]] = layernorm(e, W[o[P.P_EM_G]], W[o[P.P_EM_B]],
+                                         P.bits_f32(o[P.P_EM_EPS]))
+        elif k == P.OP_ATTENTION:
+            S, H, Dh = o[P.P_AT_SEQ], o[P.P_AT_HEADS], o[P.P_AT_DH]
+            T[o[P.P_AT_OUT]] = attention(T[o[P.P_AT_QKV]].reshape(B, S, 3 * H * Dh), H, Dh)
+        elif k == P.OP_ACT:
+            T[o[P.P_AC_OUT]] = _act(T[o[P.P_AC_IN]], o[P.P_AC_ACT])
+        elif k == P.OP_OUTPUT:
+            for j in range(o[0]):
+                t, off = o[1 + 2 * j], o[2 + 2 * j]
+                v = T[t].reshape(B, -1)
+                out[:, off:off + v.shape[1]] = v
+        else:
+            raise ValueError(f"oracle: unknown op kind {k}")
+        # keep the working precision
+        for key, val in list(T.items()):
+            if val.dtype.kind == "f" and val.dtype != dtype:
+                T[key] = val.astype(dtype)
+    return out
+
+
+def make_inputs(plan, batch: int, seed: int = 0):
+    """Host-side seeded inputs for parity runs: N(0,1) fp32 images/vectors, or
+    uniform token ids in [0, vocab)."""
+    if isinstance(plan, (bytes, bytearray)):
+        plan = P.decode(plan)
+    rng = np.random.default_rng(seed)
+    if plan.input_kind == P.IN_TOKENS:
+        vocab = next(o[P.P_TK_VOCAB] for o in plan.ops if o.kind == P.OP_TOKENS)
+        return rng.integers(0, vocab, size=(batch, plan.in_elems), dtype=np.int64)
+    return rng.standard_normal((batch, plan.in_elems), dtype=np.float32)
+
+
+def normwise_err(got, ref) -> float:
+    """max|got-ref| / max|ref| — the tolerance metric of SURVEY.md §8c."""
+    ref = np.asarray(ref, dtype=np.float64)
+    return float(np.max(np.abs(np.asarray(got, dtype=np.float64) - ref)) /
+                 max(np.max(np.abs(ref)), 1e-30))

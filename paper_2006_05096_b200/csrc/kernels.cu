@@ -1,0 +1,522 @@
+// SIMT kernels of the executor: layout packing, depthwise conv, pools,
+// LayerNorm, embedding+LN, attention, elementwise ops, output gather, the
+// seeded input generator, and the fp32 GEMM/implicit-GEMM used by fp32 plans.
+// Storage type T is float (fp32 plans) or bf16; arithmetic is fp32 throughout.
+// HBM-bound kernels map consecutive threads to the contiguous channel / feature
+// dimension so every warp access is coalesced.
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace b2 {
+
+static inline unsigned nblk(long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// ------------------------------------------------------------------ fp32 GEMM
+// 64x64 output tile, 256 threads x (4x4) outputs, K step 16; A gathered from
+// the implicit im2col view when a.conv != 0.
+template <typename T>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmSimtArgs a) {
+  __shared__ float As[16][68];
+  __shared__ float Bs[16][68];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const T* A = static_cast<const T*>(a.a);
+  const T* Wt = static_cast<const T*>(a.w);
+  // loader rows: element e = tid + i*256 -> row e>>4, k e&15 ; rows are tid>>4 + 16 i
+  int li_img[4], li_ih[4], li_iw[4];
+  bool li_ok[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + (tid >> 4) + 16 * i;
+    li_ok[i] = m < a.M;
+    li_img[i] = li_ih[i] = li_iw[i] = 0;
+    if (a.conv && li_ok[i]) {
+      const int img = m / a.OHW;
+      const int rem = m - img * a.OHW;
+      const int oh = rem / a.OW;
+      li_img[i] = img;
+      li_ih[i] = oh * a.stride - a.pad;
+      li_iw[i] = (rem - oh * a.OW) * a.stride - a.pad;
+    }
+  }
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  for (int k0 = 0; k0 < a.K; k0 += 16) {
+    const int kk = tid & 15;
+    const int k = k0 + kk;
+    int tap = 0, c = 0, r = 0, s = 0;
+    if (a.conv && k < a.K) {
+      tap = k / a.C;
+      c = k - tap * a.C;
+      r = tap / a.S;
+      s = tap - r * a.S;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = (tid >> 4) + 16 * i;
+      const int m = m0 + row;
+      float v = 0.f;
+      if (li_ok[i] && k < a.K) {
+        if (a.conv) {
+          const int ih = li_ih[i] + r, iw = li_iw[i] + s;
+          if ((unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W)
+            v = to_f(A[(((size_t)li_img[i] * a.H + ih) * a.W + iw) * a.C + c]);
+        } else {
+          v = to_f(A[(size_t)m * a.lda + k]);
+        }
+      }
+      As[kk][row] = v;
+      const int n = n0 + row;
+      Bs[kk][row] = (n < a.N && k < a.K) ? to_f(Wt[(size_t)n * a.ldw + k]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[q][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[q][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  const T* R = static_cast<const T*>(a.res);
+  T* O = static_cast<T*>(a.out);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= a.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= a.N) continue;
+      float v = acc[i][j];
+      if (a.bias) v += a.bias[n];
+      if (R) v += to_f(R[(size_t)m * a.N + n]);
+      O[(size_t)m * a.N + n] = from_f<T>(act_apply(v, a.act));
+    }
+  }
+}
+
+template <typename T> cudaError_t gemm_simt(const GemmSimtArgs& a, cudaStream_t st) {
+  dim3 grid(nblk(a.N, 64), nblk(a.M, 64));
+  gemm_simt_kernel<T><<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ packing
+template <typename T>
+__global__ void input_pack_kernel(const float* __restrict__ in, T* __restrict__ out, int B, int C,
+                                  int HW, int Cp) {
+  const long pix = (long)blockIdx.x * blockDim.x + threadIdx.x;   // over B*HW
+  if (pix >= (long)B * HW) return;
+  const long b = pix / HW, p = pix - b * HW;
+  const float* src = in + b * C * (long)HW + p;
+  T* dst = out + pix * Cp;
+  for (int c = 0; c < Cp; ++c) dst[c] = from_f<T>(c < C ? __ldg(src + (long)c * HW) : 0.f);
+}
+template <typename T>
+__global__ void vec_pack_kernel(const float* __restrict__ in, T* __restrict__ out, int B, int C,
+                                int Cp) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long)B * Cp) return;
+  const long b = i / Cp, c = i - b * Cp;
+  out[i] = from_f<T>(c < C ? in[b * C + c] : 0.f);
+}
+template <typename T>
+cudaError_t input_pack(const float* in, T* out, int B, int C, int H, int W, int Cp,
+                       cudaStream_t st) {
+  if (H * W == 1)
+    vec_pack_kernel<T><<<nblk((long)B * Cp, 256), 256, 0, st>>>(in, out, B, C, Cp);
+  else
+    input_pack_kernel<T><<<nblk((long)B * H * W, 256), 256, 0, st>>>(in, out, B, C, H * W, Cp);
+  return cudaGetLastError();
+}
+
+__global__ void tokens_kernel(const int64_t* in, int32_t* out, long n, int vocab) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  long v = in[i];
+  v = v < 0 ? 0 : (v >= vocab ? vocab - 1 : v);
+  out[i] = (int32_t)v;
+}
+cudaError_t tokens_pack(const int64_t* in, int32_t* out, long n, int vocab, cudaStream_t st) {
+  tokens_kernel<<<nblk(n, 256), 256, 0, st>>>(in, out, n, vocab);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void convert_kernel(const float* src, T* dst, long n) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = from_f<T>(src[i]);
+}
+template <typename T> cudaError_t convert_f32(const float* src, T* dst, long n, cudaStream_t st) {
+  convert_kernel<T><<<nblk(n, 256), 256, 0, st>>>(src, dst, n);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ depthwise conv
+// w_rsc: [R*R][C] (tap-major so a warp's channel loads coalesce)
+template <typename T>
+__global__ void dwconv_kernel(const T* __restrict__ x, const T* __restrict__ w,
+                              const float* __restrict__ bias, T* __restrict__ y, int B, int H,
+                              int W, int C, int R, int stride, int pad, int OH, int OW, int act) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long total = (long)B * OH * OW * C;
+  if (i >= total) return;
+  const int c = (int)(i % C);
+  long p = i / C;
+  const int ow = (int)(p % OW);
+  p /= OW;
+  const int oh = (int)(p % OH);
+  const long b = p / OH;
+  float acc = bias ? bias[c] : 0.f;
+  const int ih0 = oh * stride - pad, iw0 = ow * stride - pad;
+  for (int r = 0; r < R; ++r) {
+    const int ih = ih0 + r;
+    if ((unsigned)ih >= (unsigned)H) continue;
+    for (int s = 0; s < R; ++s) {
+      const int iw = iw0 + s;
+      if ((unsigned)iw >= (unsigned)W) continue;
+      acc = fmaf(to_f(x[((b * H + ih) * W + iw) * C + c]), to_f(w[(r * R + s) * C + c]), acc);
+    }
+  }
+  y[i] = from_f<T>(act_apply(acc, act));
+}
+template <typename T>
+cudaError_t dwconv(const T* x, const T* w, const float* bias, T* y, int B, int H, int W, int C,
+                   int R, int stride, int pad, int OH, int OW, int act, cudaStream_t st) {
+  const long total = (long)B * OH * OW * C;
+  dwconv_kernel<T><<<nblk(total, 256), 256, 0, st>>>(x, w, bias, y, B, H, W, C, R, stride, pad,
+                                                     OH, OW, act);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ pools
+template <typename T>
+__global__ void maxpool_kernel(const T* __restrict__ x, T* __restrict__ y, int B, int H, int W,
+                               int C, int k, int stride, int pad, int OH, int OW) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long total = (long)B * OH * OW * C;
+  if (i >= total) return;
+  const int c = (int)(i % C);
+  long p = i / C;
+  const int ow = (int)(p % OW);
+  p /= OW;
+  const int oh = (int)(p % OH);
+  const long b = p / OH;
+  float m = -INFINITY;
+  for (int r = 0; r < k; ++r) {
+    const int ih = oh * stride - pad + r;
+    if ((unsigned)ih >= (unsigned)H) continue;
+    for (int s = 0; s < k; ++s) {
+      const int iw = ow * stride - pad + s;
+      if ((unsigned)iw >= (unsigned)W) continue;
+      m = fmaxf(m, to_f(x[((b * H + ih) * W + iw) * C + c]));
+    }
+  }
+  y[i] = from_f<T>(m);
+}
+template <typename T>
+cudaError_t maxpool(const T* x, T* y, int B, int H, int W, int C, int k, int stride, int pad,
+                    int OH, int OW, cudaStream_t st) {
+  const long total = (long)B * OH * OW * C;
+  maxpool_kernel<T><<<nblk(total, 256), 256, 0, st>>>(x, y, B, H, W, C, k, stride, pad, OH, OW);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void avgpool_kernel(const T* __restrict__ x, T* __restrict__ y, int B, int HW, int C) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long)B * C) return;
+  const long b = i / C;
+  const int c = (int)(i - b * C);
+  const T* p = x + b * HW * (long)C + c;
+  float s = 0.f;
+  for (int q = 0; q < HW; ++q) s += to_f(p[(long)q * C]);
+  y[i] = from_f<T>(s / HW);
+}
+template <typename T>
+cudaError_t avgpool(const T* x, T* y, int B, int HW, int C, cudaStream_t st) {
+  avgpool_kernel<T><<<nblk((long)B * C, 256), 256, 0, st>>>(x, y, B, HW, C);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ LayerNorm
+B2_DEV float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// one warp per row; rows of D <= 32*32 kept in registers
+template <typename T>
+__global__ void layernorm_kernel(const T* __restrict__ x, const T* __restrict__ res,
+                                 const float* __restrict__ g, const float* __restrict__ bt,
+                                 T* __restrict__ y, long rows, int D, float eps) {
+  const long row = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const T* xr = x + row * D;
+  const T* rr = res ? res + row * D : nullptr;
+  float v[32];
+  const int per = (D + 31) / 32;
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    if (i < per) {
+      const int d = lane + 32 * i;
+      float t = 0.f;
+      if (d < D) {
+        t = to_f(xr[d]);
+        if (rr) t += to_f(rr[d]);
+      }
+      v[i] = t;
+      s += t;
+    }
+  }
+  const float mean = warp_sum(s) / D;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    if (i < per) {
+      const int d = lane + 32 * i;
+      const float t = d < D ? v[i] - mean : 0.f;
+      q += t * t;
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(q) / D + eps);
+  T* yr = y + row * D;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    if (i < per) {
+      const int d = lane + 32 * i;
+      if (d < D) yr[d] = from_f<T>((v[i] - mean) * rstd * g[d] + bt[d]);
+    }
+  }
+}
+template <typename T>
+cudaError_t layernorm(const T* x, const T* res, const float* g, const float* b, T* y, long rows,
+                      int D, float eps, cudaStream_t st) {
+  if (D > 1024) return cudaErrorInvalidValue;
+  layernorm_kernel<T><<<nblk(rows, 8), 256, 0, st>>>(x, res, g, b, y, rows, D, eps);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void embed_ln_kernel(const int32_t* __restrict__ ids, const T* __restrict__ word,
+                                const T* __restrict__ pos, const T* __restrict__ type,
+                                const float* __restrict__ g, const float* __restrict__ bt,
+                                T* __restrict__ y, int B, int S, int D, float eps) {
+  const long row = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= (long)B * S) return;
+  const int sidx = (int)(row % S);
+  const long id = ids[row];
+  float v[32];
+  const int per = (D + 31) / 32;
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    if (i < per) {
+      const int d = lane + 32 * i;
+      float t = 0.f;
+      if (d < D) t = to_f(word[id * D + d]) + to_f(pos[(long)sidx * D + d]) + to_f(type[d]);
+      v[i] = t;
+      s += t;
+    }
+  }
+  const float mean = warp_sum(s) / D;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    if (i < per) {
+      const int d = lane + 32 * i;
+      const float t = d < D ? v[i] - mean : 0.f;
+      q += t * t;
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(q) / D + eps);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    if (i < per) {
+      const int d = lane + 32 * i;
+      if (d < D) y[row * D + d] = from_f<T>((v[i] - mean) * rstd * g[d] + bt[d]);
+    }
+  }
+}
+template <typename T>
+cudaError_t embed_ln(const int32_t* ids, const T* word, const T* pos, const T* type,
+                     const float* g, const float* b, T* y, int B, int S, int D, float eps,
+                     cudaStream_t st) {
+  if (D > 1024) return cudaErrorInvalidValue;
+  embed_ln_kernel<T><<<nblk((long)B * S, 8), 256, 0, st>>>(ids, word, pos, type, g, b, y, B, S,
+                                                          D, eps);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ attention
+// One CTA per (sample, head); K and V of the head staged in shared memory as
+// fp32; each thread owns query rows and runs a single-pass online softmax.
+template <typename T, int DH>
+__global__ void attention_kernel(const T* __restrict__ qkv, T* __restrict__ out, int S, int H) {
+  extern __shared__ float kv[];
+  float* Ks = kv;
+  float* Vs = kv + S * DH;
+  const int b = blockIdx.x / H, h = blockIdx.x % H;
+  const long ld = 3L * H * DH;
+  const T* base = qkv + (long)b * S * ld;
+  for (int i = threadIdx.x; i < S * DH; i += blockDim.x) {
+    const int s = i / DH, d = i - s * DH;
+    Ks[i] = to_f(base[s * ld + (long)H * DH + h * DH + d]);
+    Vs[i] = to_f(base[s * ld + 2L * H * DH + h * DH + d]);
+  }
+  __syncthreads();
+  const float scale = rsqrtf((float)DH);
+  for (int qi = threadIdx.x; qi < S; qi += blockDim.x) {
+    float q[DH], o[DH];
+#pragma unroll
+    for (int d = 0; d < DH; ++d) {
+      q[d] = to_f(base[qi * ld + h * DH + d]) * scale;
+      o[d] = 0.f;
+    }
+    float mx = -INFINITY, sum = 0.f;
+    for (int j = 0; j < S; ++j) {
+      float sc = 0.f;
+#pragma unroll
+      for (int d = 0; d < DH; ++d) sc = fmaf(q[d], Ks[j * DH + d], sc);
+      if (sc > mx) {
+        const float corr = __expf(mx - sc);
+        sum *= corr;
+#pragma unroll
+        for (int d = 0; d < DH; ++d) o[d] *= corr;
+        mx = sc;
+      }
+      const float p = __expf(sc - mx);
+      sum += p;
+#pragma unroll
+      for (int d = 0; d < DH; ++d) o[d] = fmaf(p, Vs[j * DH + d], o[d]);
+    }
+    const float inv = 1.f / sum;
+    T* orow = out + ((long)b * S + qi) * H * DH + h * DH;
+#pragma unroll
+    for (int d = 0; d < DH; ++d) orow[d] = from_f<T>(o[d] * inv);
+  }
+}
+template <typename T>
+cudaError_t attention(const T* qkv, T* out, int B, int S, int H, int Dh, cudaStream_t st) {
+  if (Dh != 64) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)2 * S * 64 * sizeof(float);
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(attention_kernel<T, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    cfg = true;
+  }
+  attention_kernel<T, 64><<<B * H, 128, smem, st>>>(qkv, out, S, H);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ elementwise
+template <typename T>
+__global__ void act_kernel(const T* x, T* y, long n, int act) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = from_f<T>(act_apply(to_f(x[i]), act));
+}
+template <typename T> cudaError_t act_ew(const T* x, T* y, long n, int act, cudaStream_t st) {
+  act_kernel<T><<<nblk(n, 256), 256, 0, st>>>(x, y, n, act);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void output_gather_kernel(const T* src, float* out, int B, long elems, long ostride,
+                                     long off) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long)B * elems) return;
+  const long b = i / elems, e = i - b * elems;
+  out[b * ostride + off + e] = to_f(src[i]);
+}
+template <typename T>
+cudaError_t output_gather(const T* src, float* out, int B, long elems, long ostride, long off,
+                          cudaStream_t st) {
+  output_gather_kernel<T><<<nblk((long)B * elems, 256), 256, 0, st>>>(src, out, B, elems,
+                                                                      ostride, off);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ input generator
+// Counter-based: element i of stream `seed` -> splitmix64 -> Box-Muller.
+// Restated on the CPU by oracle/gen_ref.py.
+B2_DEV uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__global__ void gen_normal_kernel(float* out, long n, uint64_t seed) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t h = splitmix64(seed * 0xD1B54A32D192ED03ull + (uint64_t)i);
+  const float u1 = ((float)(h >> 40) + 1.0f) * (1.0f / 16777216.0f);
+  const float u2 = (float)((h >> 16) & 0xFFFFFFull) * (1.0f / 16777216.0f);
+  out[i] = sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+}
+__global__ void gen_tokens_kernel(int64_t* out, long n, int vocab, uint64_t seed) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t h = splitmix64(seed * 0xD1B54A32D192ED03ull + (uint64_t)i);
+  out[i] = (int64_t)(((h >> 32) * (uint64_t)vocab) >> 32);
+}
+cudaError_t gen_normal(float* out, long n, uint64_t seed, cudaStream_t st) {
+  gen_normal_kernel<<<nblk(n, 256), 256, 0, st>>>(out, n, seed);
+  return cudaGetLastError();
+}
+cudaError_t gen_tokens(int64_t* out, long n, int vocab, uint64_t seed, cudaStream_t st) {
+  gen_tokens_kernel<<<nblk(n, 256), 256, 0, st>>>(out, n, vocab, seed);
+  return cudaGetLastError();
+}
+
+__global__ void flush_kernel(uint4* p, long n, uint32_t v) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long)gridDim.x * blockDim.x)
+    p[i] = make_uint4(v, v, v, v);
+}
+cudaError_t flush_l2(void* buf, size_t bytes, cudaStream_t st) {
+  static uint32_t tick = 0;
+  flush_kernel<<<148 * 4, 256, 0, st>>>(static_cast<uint4*>(buf), (long)(bytes / 16), ++tick);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ instantiations
+#define B2_INST(T)                                                                            \
+  template cudaError_t gemm_simt<T>(const GemmSimtArgs&, cudaStream_t);                       \
+  template cudaError_t input_pack<T>(const float*, T*, int, int, int, int, int, cudaStream_t); \
+  template cudaError_t dwconv<T>(const T*, const T*, const float*, T*, int, int, int, int, int, \
+                                 int, int, int, int, int, cudaStream_t);                       \
+  template cudaError_t maxpool<T>(const T*, T*, int, int, int, int, int, int, int, int, int,   \
+                                  cudaStream_t);                                               \
+  template cudaError_t avgpool<T>(const T*, T*, int, int, int, cudaStream_t);                  \
+  template cudaError_t layernorm<T>(const T*, const T*, const float*, const float*, T*, long,  \
+                                    int, float, cudaStream_t);                                 \
+  template cudaError_t embed_ln<T>(const int32_t*, const T*, const T*, const T*, const float*, \
+                                   const float*, T*, int, int, int, float, cudaStream_t);      \
+  template cudaError_t attention<T>(const T*, T*, int, int, int, int, cudaStream_t);           \
+  template cudaError_t act_ew<T>(const T*, T*, long, int, cudaStream_t);                       \
+  template cudaError_t output_gather<T>(const T*, float*, int, long, long, long, cudaStream_t); \
+  template cudaError_t convert_f32<T>(const float*, T*, long, cudaStream_t);
+B2_INST(float)
+B2_INST(bf16)
+#undef B2_INST
+
+}  // namespace b2

@@ -1,0 +1,83 @@
+// Kernel launch interfaces used by the executor (runtime.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace b2 {
+
+// ---- tcgen05 GEMM / implicit-GEMM conv (bf16) -------------------------------
+struct TcArgs {
+  int M, N;
+  int kblocks;          // ceil(K / 64)
+  int Kreal;            // gather mode: R*S*C (chunks at k >= Kreal read as zero)
+  const float* bias;    // [N] fp32 or nullptr
+  const bf16* res;      // [M, ldres] or nullptr
+  int ldres;
+  bf16* out;            // [M, ldo]
+  int ldo;
+  int act;
+  int tiles_m, tiles_n;
+  // gather (implicit im2col) parameters, NHWC input
+  const bf16* x;
+  int H, W, C, OW, OHW, S, stride, pad;
+  int c_div64;          // C % 64 == 0 -> one filter tap per K block
+};
+
+int tc_pick_bn(long M, int N, int num_sms);
+cudaError_t tc_gemm_launch(const TcArgs& a, int bn, bool gather, const CUtensorMap& ta,
+                           const CUtensorMap& tb, int num_sms, cudaStream_t st);
+
+// ---- SIMT kernels (templated on storage type: float or bf16) -----------------
+struct GemmSimtArgs {
+  int M, N, K;          // K = real reduction length
+  const void* a;        // activations (T)
+  int lda;              // linear mode: row stride of A (elements)
+  const void* w;        // weights [N, ldw] (T)
+  int ldw;
+  const float* bias;
+  const void* res;      // [M, N] (T) or nullptr
+  void* out;            // [M, N] (T)
+  int act;
+  int conv;             // 1: implicit im2col gather from NHWC x
+  int H, W, C, OW, OHW, S, stride, pad;
+};
+
+template <typename T> cudaError_t gemm_simt(const GemmSimtArgs& a, cudaStream_t st);
+template <typename T>
+cudaError_t input_pack(const float* in, T* out, int B, int C, int H, int W, int Cp,
+                       cudaStream_t st);
+cudaError_t tokens_pack(const int64_t* in, int32_t* out, long n, int vocab, cudaStream_t st);
+template <typename T>
+cudaError_t dwconv(const T* x, const T* w_rsc, const float* bias, T* y, int B, int H, int W,
+                   int C, int R, int stride, int pad, int OH, int OW, int act, cudaStream_t st);
+template <typename T>
+cudaError_t maxpool(const T* x, T* y, int B, int H, int W, int C, int k, int stride, int pad,
+                    int OH, int OW, cudaStream_t st);
+template <typename T>
+cudaError_t avgpool(const T* x, T* y, int B, int HW, int C, cudaStream_t st);
+template <typename T>
+cudaError_t layernorm(const T* x, const T* res, const float* g, const float* b, T* y, long rows,
+                      int D, float eps, cudaStream_t st);
+template <typename T>
+cudaError_t embed_ln(const int32_t* ids, const T* word, const T* pos, const T* type,
+                     const float* g, const float* b, T* y, int B, int S, int D, float eps,
+                     cudaStream_t st);
+template <typename T>
+cudaError_t attention(const T* qkv, T* out, int B, int S, int H, int Dh, cudaStream_t st);
+template <typename T>
+cudaError_t act_ew(const T* x, T* y, long n, int act, cudaStream_t st);
+template <typename T>
+cudaError_t output_gather(const T* src, float* out, int B, long elems, long out_stride,
+                          long offset, cudaStream_t st);
+cudaError_t gen_normal(float* out, long n, uint64_t seed, cudaStream_t st);
+cudaError_t gen_tokens(int64_t* out, long n, int vocab, uint64_t seed, cudaStream_t st);
+cudaError_t flush_l2(void* buf, size_t bytes, cudaStream_t st);
+
+template <typename T>
+cudaError_t convert_f32(const float* src, T* dst, long n, cudaStream_t st);
+
+}  // namespace b2

@@ -1,0 +1,831 @@
+// libb2 executor: b200-plan parsing, weight upload in kernel layouts, per-batch
+// activation workspaces, CUDA-graph replay, and the device-timed closed-loop
+// measurement that replaces the reference profiler's host RPC timing loop
+// (pkg/src/modelci/profiler/clients.py:161-255).  C ABI in include/b2.h.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/b2.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+using namespace b2;
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(B2_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),   \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+// ------------------------------------------------------------------ plan format
+enum {
+  OP_INPUT = 1, OP_TOKENS = 2, OP_CONV = 3, OP_LINEAR = 4, OP_DWCONV = 5, OP_MAXPOOL = 6,
+  OP_AVGPOOL = 7, OP_LAYERNORM = 8, OP_EMBED = 9, OP_ATTENTION = 10, OP_OUTPUT = 11, OP_ACT = 12
+};
+constexpr int NPARAM = 31;
+
+#pragma pack(push, 1)
+struct Header {
+  char magic[4];
+  uint32_t version, dtype, n_tensors, n_weights, n_ops, input_kind, in_elems, out_elems,
+      meta_len, r0, r1;
+};
+struct TensorRec {
+  uint32_t kind, elems;
+  int32_t shape[4];
+};
+struct WeightRec {
+  uint64_t offset, numel;
+  int32_t shape[4];
+};
+struct OpRec {
+  uint32_t kind;
+  int32_t p[NPARAM];
+};
+#pragma pack(pop)
+static_assert(sizeof(Header) == 48, "header");
+static_assert(sizeof(TensorRec) == 24, "tensor rec");
+static_assert(sizeof(WeightRec) == 32, "weight rec");
+static_assert(sizeof(OpRec) == 128, "op rec");
+
+uint32_t crc32(const uint8_t* p, size_t n) {
+  static uint32_t table[256];
+  static bool init = false;
+  if (!init) {
+    for (uint32_t i = 0; i < 256; ++i) {
+      uint32_t c = i;
+      for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+      table[i] = c;
+    }
+    init = true;
+  }
+  uint32_t c = 0xFFFFFFFFu;
+  for (size_t i = 0; i < n; ++i) c = table[(c ^ p[i]) & 0xFF] ^ (c >> 8);
+  return c ^ 0xFFFFFFFFu;
+}
+
+// ------------------------------------------------------------------ TMA maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// bf16 matrix [rows, cols] with a row pitch in bytes; box = 64 cols x box_rows,
+// 128-byte swizzle (the canonical UMMA K-major layout)
+bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
+                    uint64_t row_bytes, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// ------------------------------------------------------------------ executor state
+struct Layer {
+  int kind;
+  int p[NPARAM];
+  // device parameters
+  void* w = nullptr;        // main weight in kernel layout (T)
+  float* bias = nullptr;    // fp32
+  float* g = nullptr;       // LayerNorm gamma (fp32)
+  float* b = nullptr;       // LayerNorm beta (fp32)
+  void* w2 = nullptr;       // embed: pos table (T)
+  void* w3 = nullptr;       // embed: type row (T)
+  // GEMM execution choices
+  bool tc = false, gather = false;
+  int K = 0, kpad = 0, ldw = 0;
+};
+
+struct BatchState {
+  int batch = 0;
+  std::vector<void*> act;          // per tensor
+  void* d_in = nullptr;            // internal input buffer
+  float* d_out = nullptr;          // internal output buffer
+  std::vector<int> bn;             // per layer (tc)
+  std::vector<CUtensorMap> tmA;    // per layer (tc, TMA mode)
+  std::vector<CUtensorMap> tmB;    // per layer (tc): weights, box rows = BN
+  cudaGraphExec_t graph = nullptr;
+  void* h_in = nullptr;            // pinned (e2e)
+  void* h_out = nullptr;
+};
+
+}  // namespace
+
+struct b2_plan {
+  int dtype = 1;
+  int device = 0;
+  int num_sms = 148;
+  int input_kind = 0;
+  long in_elems = 0, out_elems = 0;
+  int vocab = 0;
+  double flops = 0, weight_bytes = 0;
+  std::vector<TensorRec> tensors;
+  std::vector<Layer> layers;
+  std::vector<void*> allocs;
+  std::map<int, BatchState> states;
+  cudaStream_t stream = nullptr;
+  void* flush_buf = nullptr;
+  size_t flush_bytes = 0;
+  bool force_simt = false;
+  int launches = 0;
+};
+
+namespace {
+
+template <typename T> size_t tsize() { return sizeof(T); }
+
+int upload_f32(b2_plan* pl, const float* src, size_t n, float** out) {
+  float* d = nullptr;
+  CK(cudaMalloc(&d, n * sizeof(float) + 16));
+  pl->allocs.push_back(d);
+  CK(cudaMemcpy(d, src, n * sizeof(float), cudaMemcpyHostToDevice));
+  pl->weight_bytes += n * sizeof(float);
+  *out = d;
+  return B2_OK;
+}
+
+// host fp32 -> device T (via an fp32 staging buffer and a conversion kernel)
+template <typename T> int upload_as(b2_plan* pl, const std::vector<float>& h, void** out) {
+  float* stage = nullptr;
+  CK(cudaMalloc(&stage, h.size() * sizeof(float) + 16));
+  CK(cudaMemcpy(stage, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+  T* d = nullptr;
+  CK(cudaMalloc(&d, h.size() * sizeof(T) + 16));
+  pl->allocs.push_back(d);
+  CK(convert_f32<T>(stage, d, (long)h.size(), 0));
+  CK(cudaDeviceSynchronize());
+  CK(cudaFree(stage));
+  pl->weight_bytes += h.size() * sizeof(T);
+  *out = d;
+  return B2_OK;
+}
+
+int upload_weights(b2_plan* pl, const uint8_t* data, const std::vector<WeightRec>& wr,
+                   size_t data_len) {
+  const bool bf = pl->dtype == B2_DT_BF16;
+  auto wptr = [&](int idx, size_t* numel) -> const float* {
+    if (idx < 0 || idx >= (int)wr.size()) return nullptr;
+    if (wr[idx].offset + wr[idx].numel * 4 > data_len) return nullptr;
+    *numel = wr[idx].numel;
+    return reinterpret_cast<const float*>(data + wr[idx].offset);
+  };
+  for (Layer& L : pl->layers) {
+    size_t n = 0, nb = 0;
+    int rc = B2_OK;
+    switch (L.kind) {
+      case OP_CONV:
+      case OP_LINEAR: {
+        const bool conv = L.kind == OP_CONV;
+        const int N = conv ? L.p[7] : L.p[5];
+        const int K = conv ? L.p[8] * L.p[9] * L.p[6] : L.p[4];
+        const float* w = wptr(L.p[2], &n);
+        if (!w || n != (size_t)N * K) return fail(B2_ERR_FORMAT, "weight %d size mismatch", L.p[2]);
+        if (L.p[3] >= 0) {
+          const float* bsrc = wptr(L.p[3], &nb);
+          if (!bsrc || nb != (size_t)N) return fail(B2_ERR_FORMAT, "bias size mismatch");
+          if ((rc = upload_f32(pl, bsrc, nb, &L.bias))) return rc;
+        }
+        L.K = K;
+        const bool plain = !conv || (L.p[8] == 1 && L.p[9] == 1 && L.p[10] == 1 && L.p[11] == 0);
+        L.tc = bf && !pl->force_simt;
+        if (L.tc) {
+          const int C = conv ? L.p[6] : K;
+          if (C % 8 != 0)
+            return fail(B2_ERR_UNSUPPORTED, "bf16 %s needs channels %% 8 == 0 (got %d)",
+                        conv ? "conv" : "linear", C);
+          L.gather = !plain;
+          L.kpad = (K + 63) / 64 * 64;
+          L.ldw = L.kpad;
+          std::vector<float> h((size_t)N * L.kpad, 0.f);
+          for (int r = 0; r < N; ++r)
+            memcpy(&h[(size_t)r * L.kpad], w + (size_t)r * K, sizeof(float) * K);
+          if ((rc = upload_as<bf16>(pl, h, &L.w))) return rc;
+        } else {
+          L.ldw = K;
+          std::vector<float> h(w, w + (size_t)N * K);
+          if ((rc = bf ? upload_as<bf16>(pl, h, &L.w) : upload_as<float>(pl, h, &L.w)))
+            return rc;
+        }
+        break;
+      }
+      case OP_DWCONV: {
+        const int C = L.p[6], R = L.p[12];
+        const float* w = wptr(L.p[2], &n);
+        if (!w || n != (size_t)C * R * R) return fail(B2_ERR_FORMAT, "dw weight size mismatch");
+        std::vector<float> h((size_t)C * R * R);
+        for (int c = 0; c < C; ++c)
+          for (int t = 0; t < R * R; ++t) h[(size_t)t * C + c] = w[(size_t)c * R * R + t];
+        if ((rc = bf ? upload_as<bf16>(pl, h, &L.w) : upload_as<float>(pl, h, &L.w))) return rc;
+        if (L.p[3] >= 0) {
+          const float* bsrc = wptr(L.p[3], &nb);
+          if (!bsrc || nb != (size_t)C) return fail(B2_ERR_FORMAT, "dw bias size mismatch");
+          if ((rc = upload_f32(pl, bsrc, nb, &L.bias))) return rc;
+        }
+        break;
+      }
+      case OP_LAYERNORM: {
+        const int D = L.p[4];
+        const float* g = wptr(L.p[2], &n);
+        const float* b = wptr(L.p[3], &nb);
+        if (!g || !b || n != (size_t)D || nb != (size_t)D)
+          return fail(B2_ERR_FORMAT, "layernorm params size mismatch");
+        if ((rc = upload_f32(pl, g, n, &L.g))) return rc;
+        if ((rc = upload_f32(pl, b, nb, &L.b))) return rc;
+        break;
+      }
+      case OP_EMBED: {
+        const int D = L.p[7], S = L.p[8], V = L.p[9];
+        size_t n1, n2, n3, n4, n5;
+        const float* word = wptr(L.p[2], &n1);
+        const float* pos = wptr(L.p[3], &n2);
+        const float* typ = wptr(L.p[4], &n3);
+        const float* g = wptr(L.p[5], &n4);
+        const float* b = wptr(L.p[6], &n5);
+        if (!word || !pos || !typ || !g || !b || n1 != (size_t)V * D || n2 < (size_t)S * D ||
+            n3 != (size_t)D || n4 != (size_t)D || n5 != (size_t)D)
+          return fail(B2_ERR_FORMAT, "embedding tables size mismatch");
+        std::vector<float> h1(word, word + n1), h2(pos, pos + (size_t)S * D), h3(typ, typ + n3);
+        if (bf) {
+          if ((rc = upload_as<bf16>(pl, h1, &L.w)) || (rc = upload_as<bf16>(pl, h2, &L.w2)) ||
+              (rc = upload_as<bf16>(pl, h3, &L.w3)))
+            return rc;
+        } else {
+          if ((rc = upload_as<float>(pl, h1, &L.w)) || (rc = upload_as<float>(pl, h2, &L.w2)) ||
+              (rc = upload_as<float>(pl, h3, &L.w3)))
+            return rc;
+        }
+        if ((rc = upload_f32(pl, g, n4, &L.g)) || (rc = upload_f32(pl, b, n5, &L.b))) return rc;
+        break;
+      }
+      default:
+        break;
+    }
+  }
+  return B2_OK;
+}
+
+size_t elem_size(const b2_plan* pl, int t) {
+  if (pl->tensors[t].kind == 1) return 4;   // int32 ids
+  return pl->dtype == B2_DT_BF16 ? 2 : 4;
+}
+
+int validate_ops(b2_plan* pl) {
+  const int nt = (int)pl->tensors.size();
+  auto tok = [&](int t) { return t >= 0 && t < nt; };
+  for (size_t i = 0; i < pl->layers.size(); ++i) {
+    const Layer& L = pl->layers[i];
+    const int* p = L.p;
+    bool ok = true;
+    switch (L.kind) {
+      case OP_INPUT: ok = tok(p[0]) && p[1] > 0 && p[4] >= p[1]; break;
+      case OP_TOKENS: ok = tok(p[0]) && p[2] > 0; pl->vocab = p[2]; break;
+      case OP_CONV: ok = tok(p[0]) && tok(p[1]) && (p[15] < 0 || tok(p[15])); break;
+      case OP_LINEAR: ok = tok(p[0]) && tok(p[1]) && (p[8] < 0 || tok(p[8])); break;
+      case OP_DWCONV: case OP_MAXPOOL: case OP_AVGPOOL: case OP_ACT: ok = tok(p[0]) && tok(p[1]); break;
+      case OP_LAYERNORM: ok = tok(p[0]) && tok(p[1]) && (p[7] < 0 || tok(p[7])); break;
+      case OP_EMBED: ok = tok(p[0]) && tok(p[1]); break;
+      case OP_ATTENTION: ok = tok(p[0]) && tok(p[1]) && p[3] == 64; break;
+      case OP_OUTPUT: {
+        ok = p[0] >= 1 && p[0] <= 15;
+        for (int j = 0; ok && j < p[0]; ++j) ok = tok(p[1 + 2 * j]);
+        break;
+      }
+      default: return fail(B2_ERR_UNSUPPORTED, "op %zu: unknown kind %d", i, L.kind);
+    }
+    if (!ok) return fail(B2_ERR_FORMAT, "op %zu (kind %d): bad parameters", i, L.kind);
+  }
+  return B2_OK;
+}
+
+// ------------------------------------------------------------------ forward
+template <typename T>
+int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStream_t st,
+            cudaEvent_t* op_events) {
+  const int B = S.batch;
+  auto A = [&](int t) { return static_cast<T*>(S.act[t]); };
+  int launches = 0;
+  for (size_t li = 0; li < pl->layers.size(); ++li) {
+    Layer& L = pl->layers[li];
+    const int* p = L.p;
+    if (op_events) CK(cudaEventRecord(op_events[li], st));
+    switch (L.kind) {
+      case OP_INPUT:
+        CK(input_pack<T>(static_cast<const float*>(d_in), A(p[0]), B, p[1], p[2], p[3], p[4], st));
+        ++launches;
+        break;
+      case OP_TOKENS:
+        CK(tokens_pack(static_cast<const int64_t*>(d_in), static_cast<int32_t*>(S.act[p[0]]),
+                       (long)B * p[1], p[2], st));
+        ++launches;
+        break;
+      case OP_CONV:
+      case OP_LINEAR: {
+        const bool conv = L.kind == OP_CONV;
+        const int N = conv ? p[7] : p[5];
+        const long M = conv ? (long)B * p[12] * p[13] : (long)B * p[6];
+        const int res_t = conv ? p[15] : p[8];
+        const int act = conv ? p[14] : p[7];
+        T* out = A(p[1]);
+        if (L.tc) {
+          TcArgs a{};
+          a.M = (int)M;
+          a.N = N;
+          a.kblocks = L.kpad / 64;
+          a.Kreal = L.K;
+          a.bias = L.bias;
+          a.res = res_t >= 0 ? reinterpret_cast<const bf16*>(S.act[res_t]) : nullptr;
+          a.ldres = N;
+          a.out = reinterpret_cast<bf16*>(out);
+          a.ldo = N;
+          a.act = act;
+          const int bn = S.bn[li];
+          a.tiles_m = (int)((M + 127) / 128);
+          a.tiles_n = (N + bn - 1) / bn;
+          if (L.gather) {
+            a.x = reinterpret_cast<const bf16*>(S.act[p[0]]);
+            a.H = p[4];
+            a.W = p[5];
+            a.C = p[6];
+            a.OW = p[13];
+            a.OHW = p[12] * p[13];
+            a.S = p[9];
+            a.stride = p[10];
+            a.pad = p[11];
+            a.c_div64 = (p[6] % 64) == 0;
+          }
+          CK(tc_gemm_launch(a, bn, L.gather, L.gather ? S.tmB[li] : S.tmA[li], S.tmB[li],
+                            pl->num_sms, st));
+        } else {
+          GemmSimtArgs a{};
+          a.M = (int)M;
+          a.N = N;
+          a.K = L.K;
+          a.a = S.act[p[0]];
+          a.lda = conv ? L.K : p[9];
+          a.w = L.w;
+          a.ldw = L.ldw;
+          a.bias = L.bias;
+          a.res = res_t >= 0 ? S.act[res_t] : nullptr;
+          a.out = out;
+          a.act = act;
+          a.conv = conv && !(p[8] == 1 && p[9] == 1 && p[10] == 1 && p[11] == 0);
+          if (conv) {
+            if (!a.conv) a.lda = p[6];
+            a.H = p[4];
+            a.W = p[5];
+            a.C = p[6];
+            a.OW = p[13];
+            a.OHW = p[12] * p[13];
+            a.S = p[9];
+            a.stride = p[10];
+            a.pad = p[11];
+          }
+          CK(gemm_simt<T>(a, st));
+        }
+        ++launches;
+        break;
+      }
+      case OP_DWCONV:
+        CK(dwconv<T>(A(p[0]), static_cast<const T*>(L.w), L.bias, A(p[1]), B, p[4], p[5], p[6],
+                     p[12], p[7], p[8], p[9], p[10], p[11], st));
+        ++launches;
+        break;
+      case OP_MAXPOOL:
+        CK(maxpool<T>(A(p[0]), A(p[1]), B, p[2], p[3], p[4], p[5], p[6], p[7], p[8], p[9], st));
+        ++launches;
+        break;
+      case OP_AVGPOOL:
+        CK(avgpool<T>(A(p[0]), A(p[1]), B, p[2] * p[3], p[4], st));
+        ++launches;
+        break;
+      case OP_LAYERNORM: {
+        float eps;
+        memcpy(&eps, &p[6], 4);
+        CK(layernorm<T>(A(p[0]), p[7] >= 0 ? A(p[7]) : nullptr, L.g, L.b, A(p[1]),
+                        (long)B * p[5], p[4], eps, st));
+        ++launches;
+        break;
+      }
+      case OP_EMBED: {
+        float eps;
+        memcpy(&eps, &p[10], 4);
+        CK(embed_ln<T>(static_cast<const int32_t*>(S.act[p[0]]), static_cast<const T*>(L.w),
+                       static_cast<const T*>(L.w2), static_cast<const T*>(L.w3), L.g, L.b,
+                       A(p[1]), B, p[8], p[7], eps, st));
+        ++launches;
+        break;
+      }
+      case OP_ATTENTION:
+        CK(attention<T>(A(p[0]), A(p[1]), B, p[4], p[2], p[3], st));
+        ++launches;
+        break;
+      case OP_ACT:
+        CK(act_ew<T>(A(p[0]), A(p[1]), (long)B * p[2], p[3], st));
+        ++launches;
+        break;
+      case OP_OUTPUT:
+        for (int j = 0; j < p[0]; ++j) {
+          const int t = p[1 + 2 * j];
+          CK(output_gather<T>(A(t), d_out, B, pl->tensors[t].elems, pl->out_elems, p[2 + 2 * j],
+                              st));
+          ++launches;
+        }
+        break;
+    }
+  }
+  pl->launches = launches;
+  return B2_OK;
+}
+
+int run_forward(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStream_t st,
+                cudaEvent_t* ev = nullptr) {
+  return pl->dtype == B2_DT_BF16 ? run_ops<bf16>(pl, S, d_in, d_out, st, ev)
+                                 : run_ops<float>(pl, S, d_in, d_out, st, ev);
+}
+
+size_t in_bytes(const b2_plan* pl, int batch) {
+  return (size_t)batch * pl->in_elems * (pl->input_kind == B2_IN_TOKENS_I64 ? 8 : 4);
+}
+
+int get_state(b2_plan* pl, int batch, BatchState** out) {
+  auto it = pl->states.find(batch);
+  if (it != pl->states.end()) {
+    *out = &it->second;
+    return B2_OK;
+  }
+  BatchState S;
+  S.batch = batch;
+  S.act.resize(pl->tensors.size(), nullptr);
+  for (size_t t = 0; t < pl->tensors.size(); ++t) {
+    const size_t bytes = (size_t)batch * pl->tensors[t].elems * elem_size(pl, (int)t);
+    CK(cudaMalloc(&S.act[t], bytes + 256));
+    CK(cudaMemset(S.act[t], 0, bytes + 256));
+  }
+  CK(cudaMalloc(&S.d_in, in_bytes(pl, batch) + 256));
+  CK(cudaMemset(S.d_in, 0, in_bytes(pl, batch) + 256));
+  CK(cudaMalloc(&S.d_out, (size_t)batch * pl->out_elems * 4 + 256));
+  S.bn.assign(pl->layers.size(), 0);
+  S.tmA.resize(pl->layers.size());
+  S.tmB.resize(pl->layers.size());
+  for (size_t li = 0; li < pl->layers.size(); ++li) {
+    Layer& L = pl->layers[li];
+    if (!L.tc) continue;
+    const int* p = L.p;
+    const bool conv = L.kind == OP_CONV;
+    const int N = conv ? p[7] : p[5];
+    const long M = conv ? (long)batch * p[12] * p[13] : (long)batch * p[6];
+    const int bn = tc_pick_bn(M, N, pl->num_sms);
+    S.bn[li] = bn;
+    if (!make_tmap_bf16(&S.tmB[li], L.w, (uint64_t)N, (uint64_t)L.kpad, (uint64_t)L.kpad * 2,
+                        (uint32_t)bn))
+      return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeTiled(B) failed", li);
+    if (!L.gather) {
+      const int K = L.K;
+      const long ld = conv ? p[6] : p[9];
+      if ((ld * 2) % 16 != 0) return fail(B2_ERR_UNSUPPORTED, "layer %zu: A pitch not 16B", li);
+      if (!make_tmap_bf16(&S.tmA[li], S.act[p[0]], (uint64_t)M, (uint64_t)K, (uint64_t)ld * 2, 128))
+        return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeTiled(A) failed", li);
+    }
+  }
+  auto res = pl->states.emplace(batch, std::move(S));
+  *out = &res.first->second;
+  return B2_OK;
+}
+
+int enqueue(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStream_t st) {
+  return run_forward(pl, S, d_in, d_out, st);
+}
+
+// graph of the whole forward on the state's internal buffers
+int graph_of(b2_plan* pl, BatchState& S, cudaGraphExec_t* out) {
+  if (S.graph) {
+    *out = S.graph;
+    return B2_OK;
+  }
+  int rc;
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(pl->stream, cudaStreamCaptureModeThreadLocal));
+  rc = run_forward(pl, S, S.d_in, S.d_out, pl->stream);
+  cudaError_t e = cudaStreamEndCapture(pl->stream, &g);
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail(B2_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+  CK(cudaGraphInstantiate(&S.graph, g, 0));
+  cudaGraphDestroy(g);
+  *out = S.graph;
+  return B2_OK;
+}
+
+int gen_inputs(b2_plan* pl, void* d_in, int batch, uint64_t seed, cudaStream_t st) {
+  const long n = (long)batch * pl->in_elems;
+  if (pl->input_kind == B2_IN_TOKENS_I64) {
+    CK(gen_tokens(static_cast<int64_t*>(d_in), n, pl->vocab, seed, st));
+  } else {
+    CK(gen_normal(static_cast<float*>(d_in), n, seed, st));
+  }
+  return B2_OK;
+}
+
+int check_device(b2_plan* pl) {
+  int cur = -1;
+  CK(cudaGetDevice(&cur));
+  if (cur != pl->device) CK(cudaSetDevice(pl->device));
+  return B2_OK;
+}
+
+}  // namespace
+
+// ======================================================================= C ABI
+extern "C" {
+
+const char* b2_last_error(void) { return g_err.c_str(); }
+
+const char* b2_version(void) { return "libb2 0.1 sm_100a (tcgen05/TMA bf16, SIMT fp32)"; }
+
+int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
+  if (!blob || !out) return fail(B2_ERR_ARG, "null argument");
+  *out = nullptr;
+  const uint8_t* d = static_cast<const uint8_t*>(blob);
+  if (len < sizeof(Header) + 4) return fail(B2_ERR_FORMAT, "truncated plan");
+  Header h;
+  memcpy(&h, d, sizeof h);
+  if (memcmp(h.magic, "B2PL", 4) != 0) return fail(B2_ERR_FORMAT, "bad magic, not a b200-plan");
+  if (h.version != 1) return fail(B2_ERR_FORMAT, "unsupported plan version %u", h.version);
+  uint32_t crc;
+  memcpy(&crc, d + len - 4, 4);
+  if (crc32(d, len - 4) != crc) return fail(B2_ERR_FORMAT, "CRC mismatch, plan corrupted");
+  const size_t tables = sizeof(Header) + (size_t)h.n_tensors * sizeof(TensorRec) +
+                        (size_t)h.n_weights * sizeof(WeightRec) + (size_t)h.n_ops * sizeof(OpRec) +
+                        h.meta_len;
+  if (tables > len - 4) return fail(B2_ERR_FORMAT, "truncated plan tables");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(B2_ERR_NODEVICE, "no CUDA device visible");
+
+  b2_plan* pl = new b2_plan();
+  pl->dtype = dtype == B2_DT_FROM_PLAN ? (int)h.dtype : dtype;
+  if (pl->dtype != B2_DT_FP32 && pl->dtype != B2_DT_BF16) {
+    delete pl;
+    return fail(B2_ERR_ARG, "dtype must be 0 (fp32) or 1 (bf16)");
+  }
+  pl->input_kind = (int)h.input_kind;
+  pl->in_elems = h.in_elems;
+  pl->out_elems = h.out_elems;
+  const char* fs = getenv("B2_FORCE_SIMT");
+  pl->force_simt = fs && fs[0] == '1';
+  cudaGetDevice(&pl->device);
+  cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, pl->device);
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, pl->device);
+  if (major != 10 && pl->dtype == B2_DT_BF16 && !pl->force_simt) {
+    delete pl;
+    return fail(B2_ERR_NODEVICE, "bf16 tcgen05 path needs an sm_100 device (got sm_%d0)", major);
+  }
+  size_t pos = sizeof(Header);
+  pl->tensors.resize(h.n_tensors);
+  memcpy(pl->tensors.data(), d + pos, h.n_tensors * sizeof(TensorRec));
+  pos += h.n_tensors * sizeof(TensorRec);
+  std::vector<WeightRec> wr(h.n_weights);
+  memcpy(wr.data(), d + pos, h.n_weights * sizeof(WeightRec));
+  pos += h.n_weights * sizeof(WeightRec);
+  pl->layers.resize(h.n_ops);
+  for (uint32_t i = 0; i < h.n_ops; ++i) {
+    OpRec r;
+    memcpy(&r, d + pos, sizeof r);
+    pos += sizeof r;
+    pl->layers[i].kind = (int)r.kind;
+    memcpy(pl->layers[i].p, r.p, sizeof r.p);
+  }
+  pos += h.meta_len;
+  pos = (pos + 63) / 64 * 64;
+  if (pos > len - 4) {
+    delete pl;
+    return fail(B2_ERR_FORMAT, "truncated weight data");
+  }
+  int rc = validate_ops(pl);
+  if (!rc) rc = upload_weights(pl, d + pos, wr, len - 4 - pos);
+  if (!rc) {
+    // algorithmic FLOPs (2 per MAC) of the contraction ops
+    for (const Layer& L : pl->layers) {
+      const int* p = L.p;
+      if (L.kind == OP_CONV) pl->flops += 2.0 * p[12] * p[13] * p[7] * p[8] * p[9] * p[6];
+      if (L.kind == OP_LINEAR) pl->flops += 2.0 * p[6] * p[5] * p[4];
+      if (L.kind == OP_DWCONV) pl->flops += 2.0 * p[9] * p[10] * p[6] * p[12] * p[12];
+      if (L.kind == OP_ATTENTION) pl->flops += 4.0 * p[2] * p[4] * p[4] * p[3];
+    }
+    if (cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking) != cudaSuccess)
+      rc = fail(B2_ERR_CUDA, "cannot create stream");
+  }
+  if (rc) {
+    b2_plan_destroy(pl);
+    return rc;
+  }
+  *out = pl;
+  return B2_OK;
+}
+
+int b2_plan_io(const b2_plan* pl, int64_t* in_elems, int* in_kind, int64_t* out_elems) {
+  if (!pl) return fail(B2_ERR_ARG, "null plan");
+  if (in_elems) *in_elems = pl->in_elems;
+  if (in_kind) *in_kind = pl->input_kind;
+  if (out_elems) *out_elems = pl->out_elems;
+  return B2_OK;
+}
+
+int b2_plan_info(const b2_plan* pl, double* flops, double* wbytes, int* launches, int* dtype) {
+  if (!pl) return fail(B2_ERR_ARG, "null plan");
+  if (flops) *flops = pl->flops;
+  if (wbytes) *wbytes = pl->weight_bytes;
+  if (launches) {
+    int n = 0;
+    for (const Layer& L : pl->layers) n += L.kind == OP_OUTPUT ? L.p[0] : 1;
+    *launches = n;
+  }
+  if (dtype) *dtype = pl->dtype;
+  return B2_OK;
+}
+
+int b2_forward(b2_plan* pl, const void* d_in, void* d_out, int batch, void* stream) {
+  if (!pl || !d_in || !d_out) return fail(B2_ERR_ARG, "null argument");
+  if (batch < 1) return fail(B2_ERR_ARG, "batch must be >= 1");
+  int rc = check_device(pl);
+  if (rc) return rc;
+  BatchState* S;
+  if ((rc = get_state(pl, batch, &S))) return rc;
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : pl->stream;
+  return enqueue(pl, *S, d_in, static_cast<float*>(d_out), st);
+}
+
+int b2_forward_host(b2_plan* pl, const void* h_in, void* h_out, int batch) {
+  if (!pl || !h_in || !h_out) return fail(B2_ERR_ARG, "null argument");
+  if (batch < 1) return fail(B2_ERR_ARG, "batch must be >= 1");
+  int rc = check_device(pl);
+  if (rc) return rc;
+  BatchState* S;
+  if ((rc = get_state(pl, batch, &S))) return rc;
+  cudaGraphExec_t g;
+  if ((rc = graph_of(pl, *S, &g))) return rc;
+  CK(cudaMemcpyAsync(S->d_in, h_in, in_bytes(pl, batch), cudaMemcpyHostToDevice, pl->stream));
+  CK(cudaGraphLaunch(g, pl->stream));
+  CK(cudaMemcpyAsync(h_out, S->d_out, (size_t)batch * pl->out_elems * 4, cudaMemcpyDeviceToHost,
+                     pl->stream));
+  CK(cudaStreamSynchronize(pl->stream));
+  return B2_OK;
+}
+
+int b2_gen_input(b2_plan* pl, void* d_in, int batch, uint64_t seed, void* stream) {
+  if (!pl || !d_in || batch < 1) return fail(B2_ERR_ARG, "bad argument");
+  int rc = check_device(pl);
+  if (rc) return rc;
+  return gen_inputs(pl, d_in, batch, seed, stream ? static_cast<cudaStream_t>(stream) : pl->stream);
+}
+
+static int bench_impl(b2_plan* pl, int batch, int warmup, int n, uint64_t seed, float* lat_ms,
+                      float* completion_ms, bool e2e) {
+  if (!pl || !lat_ms || !completion_ms) return fail(B2_ERR_ARG, "null argument");
+  if (batch < 1 || n < 1 || warmup < 0) return fail(B2_ERR_ARG, "bad batch/n/warmup");
+  int rc = check_device(pl);
+  if (rc) return rc;
+  BatchState* S;
+  if ((rc = get_state(pl, batch, &S))) return rc;
+  cudaGraphExec_t g;
+  if ((rc = graph_of(pl, *S, &g))) return rc;
+  if ((rc = gen_inputs(pl, S->d_in, batch, seed, pl->stream))) return rc;
+  const size_t ib = in_bytes(pl, batch), ob = (size_t)batch * pl->out_elems * 4;
+  if (e2e && !S->h_in) {
+    CK(cudaMallocHost(&S->h_in, ib));
+    CK(cudaMallocHost(&S->h_out, ob));
+    CK(cudaMemcpyAsync(S->h_in, S->d_in, ib, cudaMemcpyDeviceToHost, pl->stream));
+  }
+  const char* fl = getenv("B2_BENCH_FLUSH_L2");
+  const bool flush = fl && fl[0] == '1';
+  if (flush && !pl->flush_buf) {
+    pl->flush_bytes = 256ull << 20;
+    CK(cudaMalloc(&pl->flush_buf, pl->flush_bytes));
+  }
+  for (int i = 0; i < warmup; ++i) {
+    if (e2e) CK(cudaMemcpyAsync(S->d_in, S->h_in, ib, cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaGraphLaunch(g, pl->stream));
+    if (e2e) CK(cudaMemcpyAsync(S->h_out, S->d_out, ob, cudaMemcpyDeviceToHost, pl->stream));
+  }
+  std::vector<cudaEvent_t> ev(2 * (size_t)n);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  for (int i = 0; i < n; ++i) {
+    if (flush) CK(flush_l2(pl->flush_buf, pl->flush_bytes, pl->stream));
+    CK(cudaEventRecord(ev[2 * i], pl->stream));
+    if (e2e) CK(cudaMemcpyAsync(S->d_in, S->h_in, ib, cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaGraphLaunch(g, pl->stream));
+    if (e2e) CK(cudaMemcpyAsync(S->h_out, S->d_out, ob, cudaMemcpyDeviceToHost, pl->stream));
+    CK(cudaEventRecord(ev[2 * i + 1], pl->stream));
+  }
+  CK(cudaStreamSynchronize(pl->stream));
+  for (int i = 0; i < n; ++i) {
+    CK(cudaEventElapsedTime(&lat_ms[i], ev[2 * i], ev[2 * i + 1]));
+    CK(cudaEventElapsedTime(&completion_ms[i], ev[0], ev[2 * i + 1]));
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return B2_OK;
+}
+
+int b2_bench(b2_plan* pl, int batch, int warmup, int n, uint64_t seed, float* lat_ms,
+             float* completion_ms) {
+  return bench_impl(pl, batch, warmup, n, seed, lat_ms, completion_ms, false);
+}
+
+int b2_bench_e2e(b2_plan* pl, int batch, int warmup, int n, uint64_t seed, float* lat_ms,
+                 float* completion_ms) {
+  return bench_impl(pl, batch, warmup, n, seed, lat_ms, completion_ms, true);
+}
+
+int b2_profile_ops(b2_plan* pl, int batch, int iters, float* op_ms, int* n_ops, int* op_kinds) {
+  if (!pl || !op_ms || !n_ops || batch < 1 || iters < 1) return fail(B2_ERR_ARG, "bad argument");
+  int rc = check_device(pl);
+  if (rc) return rc;
+  BatchState* S;
+  if ((rc = get_state(pl, batch, &S))) return rc;
+  if ((rc = gen_inputs(pl, S->d_in, batch, 1234, pl->stream))) return rc;
+  const size_t nl = pl->layers.size();
+  std::vector<cudaEvent_t> ev(nl + 1);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  std::vector<double> acc(nl, 0.0);
+  for (int it = 0; it <= iters; ++it) {   // iteration 0 is a warm-up
+    if ((rc = run_forward(pl, *S, S->d_in, S->d_out, pl->stream, ev.data()))) return rc;
+    CK(cudaEventRecord(ev[nl], pl->stream));
+    CK(cudaStreamSynchronize(pl->stream));
+    if (it == 0) continue;
+    for (size_t i = 0; i < nl; ++i) {
+      float ms;
+      CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      acc[i] += ms;
+    }
+  }
+  for (size_t i = 0; i < nl; ++i) {
+    op_ms[i] = (float)(acc[i] / iters);
+    if (op_kinds) op_kinds[i] = pl->layers[i].kind;
+  }
+  *n_ops = (int)nl;
+  for (auto& e : ev) cudaEventDestroy(e);
+  return B2_OK;
+}
+
+void b2_plan_destroy(b2_plan* pl) {
+  if (!pl) return;
+  cudaSetDevice(pl->device);
+  if (pl->stream) cudaStreamSynchronize(pl->stream);
+  for (auto& kv : pl->states) {
+    BatchState& S = kv.second;
+    if (S.graph) cudaGraphExecDestroy(S.graph);
+    for (void* p : S.act) cudaFree(p);
+    cudaFree(S.d_in);
+    cudaFree(S.d_out);
+    if (S.h_in) cudaFreeHost(S.h_in);
+    if (S.h_out) cudaFreeHost(S.h_out);
+  }
+  for (void* p : pl->allocs) cudaFree(p);
+  if (pl->flush_buf) cudaFree(pl->flush_buf);
+  if (pl->stream) cudaStreamDestroy(pl->stream);
+  delete pl;
+}
+
+}  // extern "C"
