@@ -1,0 +1,304 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 profiling hot path (the driver's contract).
+
+One step = one pass of the hot path over one batch: a ResNet-50 bf16 forward
+at batch 256 (BASELINE.json configs[1], the largest single-GPU profile cell),
+replayed from a CUDA graph inside libb2 with inputs resident in HBM, timed
+with CUDA events (``b2_bench``).  ``e2e`` is the same metric through the
+C-ABI call with HOST buffers (``b2_bench_e2e``: pinned H2D of the fp32 input
+batch, forward, D2H of the logits, every step).
+
+Multi-GPU (torchrun): one process per GPU, each runs its own replica of the
+step (the sweep shards by cell with no data-path collective: "scaling": weak);
+a barrier + max-over-ranks brackets the timed region.
+
+``--impl reference`` times the CPU implementation of the path (the numpy
+oracle port of the forward, oracle/plan_ref.py, on all host cores) on a
+bounded sample of the same workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "samples/s & p50/p99 latency per batch size; profile-sweep wall time 1-8 GPU"
+UNIT = "samples/s"
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
+            int(os.environ.get("WORLD_SIZE", "1")))
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        d["_source"] = "measured"
+        return d
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "_source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self._halt = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._halt.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout
+                for line in out.strip().splitlines():
+                    self.rows.append([c.strip() for c in line.split(",")])
+            except Exception:
+                return
+            self._halt.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._halt.set()
+        self._t.join(timeout=6)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        busy = [r for r in self.rows if r[6].isdigit() and int(r[6]) > 0] or self.rows
+        sm = [float(r[0]) for r in busy if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in busy for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].isdigit() else None,
+                "reasons": reasons, "samples": len(busy)}
+
+
+def build_plan(model: str, dtype: int) -> bytes:
+    from paper_2006_05096_b200 import zoo
+    return zoo.build_plan(model, dtype, seed=0)
+
+
+def cpu_baseline(model: str, plan_bytes: bytes, seconds: float = 12.0, batch: int = 4) -> dict:
+    """The oracle port (numpy fp32 forward, all host threads) on a bounded
+    sample: `batch`-sample forwards repeated for ~`seconds`."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import numpy as np
+    import plan_ref
+    from paper_2006_05096_b200 import plan as P
+    pl = P.decode(plan_bytes)
+    x = plan_ref.make_inputs(pl, batch, 0)
+    plan_ref.forward(pl, x, np.float32)   # warm-up (BLAS threads, page-in)
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        plan_ref.forward(pl, x, np.float32)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or n >= 50:
+            break
+    return {"value": n * batch / el, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{n} x {model} fp32 forwards of batch {batch} (numpy oracle, "
+                      f"{el:.1f} s)"}
+
+
+def roofline(plan, plan_bytes: bytes, batch: int, pk: dict) -> dict:
+    """Dominant kernel = the tcgen05 GEMM/implicit-GEMM (every conv/linear op).
+    achieved = algorithmic FLOPs of those launches / their summed CUDA-event
+    durations (per-op events on the plan's stream, eager replay)."""
+    from paper_2006_05096_b200 import plan as P
+    pl = P.decode(plan_bytes)
+    prof = plan.profile_ops(batch, iters=3)
+    fl = 0.0
+    t_gemm = 0.0
+    t_all = 0.0
+    launches = 0
+    for o, (_, ms) in zip(pl.ops, prof):
+        t_all += ms
+        if o.kind == P.OP_CONV:
+            fl += 2.0 * o[12] * o[13] * o[7] * o[8] * o[9] * o[6] * batch
+        elif o.kind == P.OP_LINEAR:
+            fl += 2.0 * o[6] * o[5] * o[4] * batch
+        else:
+            continue
+        t_gemm += ms
+        launches += 1
+    achieved = fl / (t_gemm / 1e3) / 1e12
+    peak = pk.get("bf16_tflops_sustained", 1400.0)
+    traffic = None
+    tp = ROOT / "profiles" / "ncu_traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get("tc_gemm_bytes_per_launch")
+    return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "kernel": "b2::tc_gemm_kernel (tcgen05 GEMM / implicit-GEMM conv)",
+            "launches_per_step": launches, "avg_launch_ms": round(t_gemm / launches, 5),
+            "share_of_step": round(t_gemm / t_all, 4),
+            "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({pk['_source']})"}
+
+
+def run_ours(args) -> dict | None:
+    rank, local, world = dist_env()
+    if world > 1:
+        os.environ.setdefault("CUDA_VISIBLE_DEVICES", str(local))
+    import numpy as np
+    from paper_2006_05096_b200 import plan as P, runtime as R
+    dt = P.DT_BF16 if args.dtype == "bf16" else P.DT_FP32
+    pg = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        pg = dist
+    blob = build_plan(args.model, dt)
+    plan = R.Plan(blob, dt)
+    B, K, W = args.batch, args.steps, args.warmup
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if pg is None:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64,
+                         device="cuda" if torch.cuda.is_available() else "cpu")
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return float(t.item())
+
+    # device-resident timed region: K graph replays bracketed by CUDA events
+    plan.bench(B, 2, 1, seed=1)               # build workspaces + graph outside the region
+    barrier()
+    with ClockSampler(0 if world > 1 else int(os.environ.get("B2_GPU_INDEX", "0"))) as clk:
+        lat, comp = plan.bench(B, K, W, seed=0)
+    barrier()
+    elapsed_ms = max_over_ranks(float(comp[-1]))
+    value = world * K * B / (elapsed_ms / 1e3)
+    # end-to-end through the C ABI with host buffers (pinned H2D + D2H per step)
+    plan.bench(B, 1, 1, seed=2, e2e=True)
+    barrier()
+    elat, ecomp = plan.bench(B, K, W, seed=0, e2e=True)
+    barrier()
+    e2e_ms = max_over_ranks(float(ecomp[-1]))
+    e2e_value = world * K * B / (e2e_ms / 1e3)
+    if rank != 0:
+        if pg is not None:
+            pg.destroy_process_group()
+        return None
+    pk = peaks()
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(elapsed_ms / K, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": args.dtype, "data": "synthetic (seeded N(0,1) images; seeded random-init "
+                                     "weights, BN calibrated)",
+        "config": {"workload": f"{args.model} {args.dtype} profile cell, batch {B} "
+                               "(BASELINE configs[1])", "model": args.model,
+                   "global_batch": B * world, "seq_len": None,
+                   "parallelism": f"replicas x{world} (cells shard, no collective)",
+                   "l2": "inputs larger than L2 (fp32 input batch %.0f MB + activations)"
+                         % (B * plan.in_elems * 4 / 1e6)},
+        "p50_ms": round(float(np.percentile(lat, 50)), 4),
+        "p99_ms": round(float(np.percentile(lat, 99)), 4),
+        "e2e": {"value": round(e2e_value, 1), "unit": UNIT,
+                "h2d_bytes_per_step": int(B * plan.in_elems * 4),
+                "d2h_bytes_per_step": int(B * plan.out_elems * 4),
+                "ms_per_step": round(e2e_ms / K, 4)},
+        "gpu_launches": int(K * plan.launches_per_forward),
+        "clocks": clk.summary(),
+    }
+    line["roofline"] = roofline(plan, blob, B, pk)
+    if not args.no_sweep:
+        table = {}
+        for b in (1, 2, 4, 8, 16, 32, 64, 128, 256):
+            l, c = plan.bench(b, 20, 3, seed=b)
+            table[str(b)] = {"samples_s": round(20 * b / (float(c[-1]) / 1e3), 1),
+                             "p50_ms": round(float(np.percentile(l, 50)), 4),
+                             "p99_ms": round(float(np.percentile(l, 99)), 4)}
+        line["per_batch"] = table
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(args.model, blob)
+    if pg is not None:
+        pg.destroy_process_group()
+    return line
+
+
+def run_reference(args) -> dict | None:
+    rank, _, world = dist_env()
+    if rank != 0:
+        return None
+    from paper_2006_05096_b200 import plan as P
+    blob = build_plan(args.model, P.DT_FP32)
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import numpy as np
+    import plan_ref
+    pl = P.decode(blob)
+    sample = 4   # bounded per-step sample of the batch-256 workload
+    x = plan_ref.make_inputs(pl, sample, 0)
+    for _ in range(args.warmup):
+        plan_ref.forward(pl, x, np.float32)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        plan_ref.forward(pl, x, np.float32)
+    el = time.perf_counter() - t0
+    value = args.steps * sample / el
+    cb = {"value": round(value, 3), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+          "sample": f"{sample} of the {args.batch}-sample batch per step, numpy fp32 oracle "
+                    f"forward of {args.model} on all host threads"}
+    return {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(el / args.steps * 1e3, 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{args.model} profile cell, batch {args.batch} "
+                                   f"(CPU: {sample}-sample bounded step)", "model": args.model,
+                       "global_batch": args.batch, "seq_len": None, "parallelism": "cpu"},
+            "cpu_baseline": cb,
+            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--model", default="resnet50")
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--dtype", choices=["bf16", "fp32"], default="bf16")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

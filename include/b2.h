@@ -33,6 +33,12 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define B2_API __attribute__((visibility("default")))
+#else
+#define B2_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -58,54 +64,59 @@ typedef struct b2_plan b2_plan;
 
 /* Parse a b200-plan blob, upload weights in kernel layouts (bf16 K-major
  * tiles for tcgen05, or fp32), and bind the plan to the current device. */
-int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out);
+B2_API int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out);
 
 /* Per-sample element counts and the input element type. */
-int b2_plan_io(const b2_plan* plan, int64_t* in_elems_per_sample, int* in_kind,
+B2_API int b2_plan_io(const b2_plan* plan, int64_t* in_elems_per_sample, int* in_kind,
                int64_t* out_elems_per_sample);
 
 /* Model facts: algorithmic FLOPs per sample, weight bytes resident in HBM,
  * number of kernel launches one forward issues. */
-int b2_plan_info(const b2_plan* plan, double* flops_per_sample, double* weight_bytes,
+B2_API int b2_plan_info(const b2_plan* plan, double* flops_per_sample, double* weight_bytes,
                  int* launches_per_forward, int* dtype);
 
 /* One forward on device buffers: d_in [batch, in_elems] (f32 or i64),
  * d_out [batch, out_elems] f32.  Enqueued on `stream` (NULL = the plan's
  * stream); the call does not synchronise. */
-int b2_forward(b2_plan* plan, const void* d_in, void* d_out, int batch, void* stream);
+B2_API int b2_forward(b2_plan* plan, const void* d_in, void* d_out, int batch, void* stream);
 
 /* Host buffers in and out: H2D copy, forward, D2H copy, synchronised. */
-int b2_forward_host(b2_plan* plan, const void* h_in, void* h_out, int batch);
+B2_API int b2_forward_host(b2_plan* plan, const void* h_in, void* h_out, int batch);
 
 /* Closed-loop device-timed measurement of one sweep cell: `warmup` untimed
  * forwards then `n` timed ones on device-resident seeded inputs, each replayed
  * from a CUDA graph and bracketed by CUDA events.  lat_ms[i] is request i's
  * device time, completion_ms[i] its completion instant since the first
  * request started (host arrays of n floats). */
-int b2_bench(b2_plan* plan, int batch, int warmup, int n, uint64_t seed, float* lat_ms,
+B2_API int b2_bench(b2_plan* plan, int batch, int warmup, int n, uint64_t seed, float* lat_ms,
              float* completion_ms);
 
 /* Same loop but every request goes host->device->host through pinned buffers
  * (the end-to-end view a remote client sees); inputs regenerated per seed. */
-int b2_bench_e2e(b2_plan* plan, int batch, int warmup, int n, uint64_t seed, float* lat_ms,
+B2_API int b2_bench_e2e(b2_plan* plan, int batch, int warmup, int n, uint64_t seed, float* lat_ms,
                  float* completion_ms);
 
 /* Seeded synthetic inputs written to a device buffer (N(0,1) f32 or uniform
  * token ids) — the device-side build_payload. */
-int b2_gen_input(b2_plan* plan, void* d_in, int batch, uint64_t seed, void* stream);
+B2_API int b2_gen_input(b2_plan* plan, void* d_in, int batch, uint64_t seed, void* stream);
 
 /* Per-op device times (ms) of one forward at `batch`, averaged over `iters`
  * eager runs: op_ms[i] for op i (n_ops entries; returns the count in *n_ops). */
-int b2_profile_ops(b2_plan* plan, int batch, int iters, float* op_ms, int* n_ops,
+B2_API int b2_profile_ops(b2_plan* plan, int batch, int iters, float* op_ms, int* n_ops,
                    int* op_kinds);
 
-void b2_plan_destroy(b2_plan* plan);
+/* Copy activation tensor `tensor` (as stored: bf16/fp32, or int32 ids) of the
+ * last forward run at `batch` into host memory (verification hook: lets the
+ * parity tests check every op against the oracle on the kernel's own inputs). */
+B2_API int b2_read_tensor(b2_plan* plan, int batch, int tensor, void* host_out, size_t bytes);
+
+B2_API void b2_plan_destroy(b2_plan* plan);
 
 /* Thread-local message for the last nonzero status. */
-const char* b2_last_error(void);
+B2_API const char* b2_last_error(void);
 
 /* Library build string (arch, git-free version). */
-const char* b2_version(void);
+B2_API const char* b2_version(void);
 
 #ifdef __cplusplus
 }

@@ -121,88 +121,134 @@ def attention(qkv, heads, dh):
     return (p @ v).transpose(0, 2, 1, 3).reshape(B, S, heads * dh)
 
 
-def forward(plan, x, dtype=np.float64):
-    """Run a decoded plan (plan.decode) on a host batch.
+def round_bf16(x):
+    """Round-to-nearest-even to bfloat16, returned as float32 (the kernels'
+    __float2bfloat16_rn)."""
+    a = np.array(x, dtype=np.float32, copy=True)
+    u = a.view(np.uint32)
+    u += np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))
+    u &= np.uint32(0xFFFF0000)
+    return a
 
-    ``x``: dense inputs [B, in_elems] (float) or token ids [B, seq] (int).
-    Returns the fp output [B, out_elems] in ``dtype``.
-    """
-    if isinstance(plan, (bytes, bytearray)):
-        plan = P.decode(plan)
-    W = [w.astype(dtype) for w in plan.weights]
-    B = x.shape[0]
-    T: dict[int, np.ndarray] = {}
 
+def bf16_weight_ids(plan) -> set:
+    """Weights the bf16 executor stores as bf16 (contraction weights and
+    embedding tables); biases and LayerNorm affine stay fp32."""
+    ids = set()
+    for o in plan.ops:
+        if o.kind in (P.OP_CONV, P.OP_LINEAR, P.OP_DWCONV):
+            ids.add(o[2])
+        elif o.kind == P.OP_EMBED:
+            ids |= {o[P.P_EM_WORD], o[P.P_EM_POS], o[P.P_EM_TYPE]}
+    return ids
+
+
+class _Bf16Store(dict):
+    """Activation store that rounds every floating tensor to bf16 on write —
+    the rounding points of the bf16 executor (each op reads bf16, computes in
+    fp32, writes bf16)."""
+
+    def __setitem__(self, k, v):
+        if v.dtype.kind == "f":
+            v = round_bf16(v).astype(np.float64)
+        super().__setitem__(k, v)
+
+
+def run_op(plan, o, T, W, B, x, out, dtype=np.float64):
+    """Execute one plan op on the host tensors ``T`` (dict tensor -> array)."""
     def shaped(t):
         return T[t].reshape((B,) + plan.tensors[t].shape)
 
     def wt(i):
         return None if i < 0 else W[i]
 
+    k = o.kind
+    if k == P.OP_INPUT:
+        C, H, Wd, Cp = o[P.P_IN_C], o[P.P_IN_H], o[P.P_IN_W], o[P.P_IN_CPAD]
+        img = np.asarray(x, dtype=dtype).reshape(B, C, H, Wd).transpose(0, 2, 3, 1)
+        buf = np.zeros((B, H, Wd, Cp), dtype=dtype)
+        buf[..., :C] = img
+        T[o[P.P_IN_OUT]] = buf
+    elif k == P.OP_TOKENS:
+        T[o[P.P_TK_OUT]] = np.asarray(x, dtype=np.int64).reshape(B, o[P.P_TK_SEQ])
+    elif k == P.OP_CONV:
+        y = conv2d_nhwc(shaped(o[P.P_CV_IN]), W[o[P.P_CV_W]], wt(o[P.P_CV_B]),
+                        o[P.P_CV_STRIDE], o[P.P_CV_PAD])
+        if o[P.P_CV_RES] >= 0:
+            y = y + shaped(o[P.P_CV_RES])
+        T[o[P.P_CV_OUT]] = _act(y, o[P.P_CV_ACT])
+    elif k == P.OP_LINEAR:
+        K, N, rows, astride = o[P.P_LN_K], o[P.P_LN_N], o[P.P_LN_ROWS], o[P.P_LN_ASTRIDE]
+        flat = T[o[P.P_LN_IN]].reshape(B, -1)
+        idx = np.arange(rows)[:, None] * astride + np.arange(K)[None, :]
+        a = flat[:, idx]                                     # [B, rows, K]
+        y = a @ W[o[P.P_LN_W]].T
+        if o[P.P_LN_B] >= 0:
+            y = y + W[o[P.P_LN_B]]
+        if o[P.P_LN_RES] >= 0:
+            y = y + T[o[P.P_LN_RES]].reshape(B, rows, N)
+        T[o[P.P_LN_OUT]] = _act(y, o[P.P_LN_ACT])
+    elif k == P.OP_DWCONV:
+        y = dwconv_nhwc(shaped(o[P.P_DW_IN]), W[o[P.P_DW_W]], wt(o[P.P_DW_B]),
+                        o[P.P_DW_STRIDE], o[P.P_DW_PAD])
+        T[o[P.P_DW_OUT]] = _act(y, o[P.P_DW_ACT])
+    elif k == P.OP_MAXPOOL:
+        T[o[P.P_MP_OUT]] = maxpool_nhwc(shaped(o[P.P_MP_IN]), o[P.P_MP_K],
+                                        o[P.P_MP_STRIDE], o[P.P_MP_PAD])
+    elif k == P.OP_AVGPOOL:
+        T[o[P.P_AP_OUT]] = shaped(o[P.P_AP_IN]).mean(axis=(1, 2))
+    elif k == P.OP_LAYERNORM:
+        D, rows = o[P.P_LNM_D], o[P.P_LNM_ROWS]
+        v = T[o[P.P_LNM_IN]].reshape(B, rows, D)
+        if o[P.P_LNM_RES] >= 0:
+            v = v + T[o[P.P_LNM_RES]].reshape(B, rows, D)
+        T[o[P.P_LNM_OUT]] = layernorm(v, W[o[P.P_LNM_G]], W[o[P.P_LNM_B]],
+                                      P.bits_f32(o[P.P_LNM_EPS]))
+    elif k == P.OP_EMBED:
+        ids = T[o[P.P_EM_IDS]]
+        e = W[o[P.P_EM_WORD]][ids] + W[o[P.P_EM_POS]][None, :ids.shape[1]] + \
+            W[o[P.P_EM_TYPE]][None, None, :]
+        T[o[P.P_EM_OUT]] = layernorm(e, W[o[P.P_EM_G]], W[o[P.P_EM_B]],
+                                     P.bits_f32(o[P.P_EM_EPS]))
+    elif k == P.OP_ATTENTION:
+        S, H, Dh = o[P.P_AT_SEQ], o[P.P_AT_HEADS], o[P.P_AT_DH]
+        T[o[P.P_AT_OUT]] = attention(T[o[P.P_AT_QKV]].reshape(B, S, 3 * H * Dh), H, Dh)
+    elif k == P.OP_ACT:
+        T[o[P.P_AC_OUT]] = _act(T[o[P.P_AC_IN]], o[P.P_AC_ACT])
+    elif k == P.OP_OUTPUT:
+        for j in range(o[0]):
+            t, off = o[1 + 2 * j], o[2 + 2 * j]
+            v = T[t].reshape(B, -1)
+            out[:, off:off + v.shape[1]] = v
+    else:
+        raise ValueError(f"oracle: unknown op kind {k}")
+
+
+def forward(plan, x, dtype=np.float64, emulate_bf16: bool = False):
+    """Run a decoded plan (plan.decode) on a host batch.
+
+    ``x``: dense inputs [B, in_elems] (float) or token ids [B, seq] (int).
+    Returns the fp output [B, out_elems] in ``dtype``.  ``emulate_bf16``
+    reproduces the bf16 executor's rounding points (bf16 weights and
+    activations, fp32 biases/affines, wide accumulation) so bf16 kernels can be
+    checked against their own arithmetic rather than against fp32.
+    """
+    if isinstance(plan, (bytes, bytearray)):
+        plan = P.decode(plan)
+    if emulate_bf16:
+        dtype = np.float64
+        keep = bf16_weight_ids(plan)
+        W = [round_bf16(w).astype(dtype) if i in keep else w.astype(dtype)
+             for i, w in enumerate(plan.weights)]
+    else:
+        W = [w.astype(dtype) for w in plan.weights]
+    B = x.shape[0]
+    T: dict[int, np.ndarray] = _Bf16Store() if emulate_bf16 else {}
+
     out = np.zeros((B, plan.out_elems), dtype=dtype)
     for o in plan.ops:
-        k = o.kind
-        if k == P.OP_INPUT:
-            C, H, Wd, Cp = o[P.P_IN_C], o[P.P_IN_H], o[P.P_IN_W], o[P.P_IN_CPAD]
-            img = np.asarray(x, dtype=dtype).reshape(B, C, H, Wd).transpose(0, 2, 3, 1)
-            buf = np.zeros((B, H, Wd, Cp), dtype=dtype)
-            buf[..., :C] = img
-            T[o[P.P_IN_OUT]] = buf
-        elif k == P.OP_TOKENS:
-            T[o[P.P_TK_OUT]] = np.asarray(x, dtype=np.int64).reshape(B, o[P.P_TK_SEQ])
-        elif k == P.OP_CONV:
-            y = conv2d_nhwc(shaped(o[P.P_CV_IN]), W[o[P.P_CV_W]], wt(o[P.P_CV_B]),
-                            o[P.P_CV_STRIDE], o[P.P_CV_PAD])
-            if o[P.P_CV_RES] >= 0:
-                y = y + shaped(o[P.P_CV_RES])
-            T[o[P.P_CV_OUT]] = _act(y, o[P.P_CV_ACT])
-        elif k == P.OP_LINEAR:
-            K, N, rows, astride = o[P.P_LN_K], o[P.P_LN_N], o[P.P_LN_ROWS], o[P.P_LN_ASTRIDE]
-            flat = T[o[P.P_LN_IN]].reshape(B, -1)
-            idx = np.arange(rows)[:, None] * astride + np.arange(K)[None, :]
-            a = flat[:, idx]                                     # [B, rows, K]
-            y = a @ W[o[P.P_LN_W]].T
-            if o[P.P_LN_B] >= 0:
-                y = y + W[o[P.P_LN_B]]
-            if o[P.P_LN_RES] >= 0:
-                y = y + T[o[P.P_LN_RES]].reshape(B, rows, N)
-            T[o[P.P_LN_OUT]] = _act(y, o[P.P_LN_ACT])
-        elif k == P.OP_DWCONV:
-            y = dwconv_nhwc(shaped(o[P.P_DW_IN]), W[o[P.P_DW_W]], wt(o[P.P_DW_B]),
-                            o[P.P_DW_STRIDE], o[P.P_DW_PAD])
-            T[o[P.P_DW_OUT]] = _act(y, o[P.P_DW_ACT])
-        elif k == P.OP_MAXPOOL:
-            T[o[P.P_MP_OUT]] = maxpool_nhwc(shaped(o[P.P_MP_IN]), o[P.P_MP_K],
-                                            o[P.P_MP_STRIDE], o[P.P_MP_PAD])
-        elif k == P.OP_AVGPOOL:
-            T[o[P.P_AP_OUT]] = shaped(o[P.P_AP_IN]).mean(axis=(1, 2))
-        elif k == P.OP_LAYERNORM:
-            D, rows = o[P.P_LNM_D], o[P.P_LNM_ROWS]
-            v = T[o[P.P_LNM_IN]].reshape(B, rows, D)
-            if o[P.P_LNM_RES] >= 0:
-                v = v + T[o[P.P_LNM_RES]].reshape(B, rows, D)
-            T[o[P.P_LNM_OUT]] = layernorm(v, W[o[P.P_LNM_G]], W[o[P.P_LNM_B]],
-                                          P.bits_f32(o[P.P_LNM_EPS]))
-        elif k == P.OP_EMBED:
-            ids = T[o[P.P_EM_IDS]]
-            e = W[o[P.P_EM_WORD]][ids] + W[o[P.P_EM_POS]][None, :ids.shape[1]] + \
-                W[o[P.P_EM_TYPE]][None, None, :]
-            T[o[P.P_EM_OUT]] = layernorm(e, W[o[P.P_EM_G]], W[o[P.P_EM_B]],
-                                         P.bits_f32(o[P.P_EM_EPS]))
-        elif k == P.OP_ATTENTION:
-            S, H, Dh = o[P.P_AT_SEQ], o[P.P_AT_HEADS], o[P.P_AT_DH]
-            T[o[P.P_AT_OUT]] = attention(T[o[P.P_AT_QKV]].reshape(B, S, 3 * H * Dh), H, Dh)
-        elif k == P.OP_ACT:
-            T[o[P.P_AC_OUT]] = _act(T[o[P.P_AC_IN]], o[P.P_AC_ACT])
-        elif k == P.OP_OUTPUT:
-            for j in range(o[0]):
-                t, off = o[1 + 2 * j], o[2 + 2 * j]
-                v = T[t].reshape(B, -1)
-                out[:, off:off + v.shape[1]] = v
-        else:
-            raise ValueError(f"oracle: unknown op kind {k}")
-        # keep the working precision
-        for key, val in list(T.items()):
+        run_op(plan, o, T, W, B, x, out, dtype)
+        for key, val in list(T.items()):   # keep the working precision
             if val.dtype.kind == "f" and val.dtype != dtype:
                 T[key] = val.astype(dtype)
     return out
@@ -225,3 +271,58 @@ def normwise_err(got, ref) -> float:
     ref = np.asarray(ref, dtype=np.float64)
     return float(np.max(np.abs(np.asarray(got, dtype=np.float64) - ref)) /
                  max(np.max(np.abs(ref)), 1e-30))
+
+
+def op_io(o):
+    """(input tensor ids, output tensor id) of an op (OUTPUT: no output)."""
+    k = o.kind
+    if k in (P.OP_INPUT, P.OP_TOKENS):
+        return [], o[0]
+    if k == P.OP_CONV:
+        return [o[P.P_CV_IN]] + ([o[P.P_CV_RES]] if o[P.P_CV_RES] >= 0 else []), o[P.P_CV_OUT]
+    if k == P.OP_LINEAR:
+        return [o[P.P_LN_IN]] + ([o[P.P_LN_RES]] if o[P.P_LN_RES] >= 0 else []), o[P.P_LN_OUT]
+    if k == P.OP_LAYERNORM:
+        return [o[P.P_LNM_IN]] + ([o[P.P_LNM_RES]] if o[P.P_LNM_RES] >= 0 else []), o[1]
+    if k == P.OP_OUTPUT:
+        return [o[1 + 2 * j] for j in range(o[0])], None
+    return [o[0]], o[1]
+
+
+def layerwise_errors(plan, read_tensor, x, emulate_bf16: bool):
+    """Teacher-forced per-op parity.
+
+    Every op is recomputed on the host from the executor's OWN input tensors
+    (``read_tensor(t) -> float64/int array`` after a device forward on ``x``)
+    and compared with the executor's output tensor.  Unlike an end-to-end
+    comparison this does not amplify rounding through a deep network, so the
+    bound is one rounding of the op's own output.  Returns [(op_index, name,
+    normwise_err)].
+    """
+    if isinstance(plan, (bytes, bytearray)):
+        plan = P.decode(plan)
+    B = x.shape[0]
+    if emulate_bf16:
+        keep = bf16_weight_ids(plan)
+        W = [round_bf16(w).astype(np.float64) if i in keep else w.astype(np.float64)
+             for i, w in enumerate(plan.weights)]
+    else:
+        W = [w.astype(np.float64) for w in plan.weights]
+    out = np.zeros((B, plan.out_elems))
+    res = []
+    for i, o in enumerate(plan.ops):
+        ins, dst = op_io(o)
+        if dst is None:
+            continue
+        T = _Bf16Store() if emulate_bf16 else {}
+        for t in ins:
+            v = read_tensor(t)
+            if plan.tensors[t].kind == P.T_IDS:
+                dict.__setitem__(T, t, np.asarray(v, dtype=np.int64).reshape(B, -1))
+            else:
+                dict.__setitem__(T, t, np.asarray(v, dtype=np.float64))
+        run_op(plan, o, T, W, B, x, out, np.float64)
+        ref = np.asarray(T[dst], dtype=np.float64).reshape(B, -1)
+        got = np.asarray(read_tensor(dst), dtype=np.float64).reshape(B, -1)
+        res.append((i, o.name, normwise_err(got, ref)))
+    return res

@@ -11,6 +11,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #define B2_DEV __device__ __forceinline__
 
@@ -26,6 +27,14 @@ B2_DEV float act_apply(float v, int act) {
     case ACT_TANH: return tanhf(v);
     default: return v;
   }
+}
+
+template <int ACT> B2_DEV float act_t(float v) {
+  if constexpr (ACT == ACT_RELU) return fmaxf(v, 0.f);
+  else if constexpr (ACT == ACT_RELU6) return fminf(fmaxf(v, 0.f), 6.f);
+  else if constexpr (ACT == ACT_GELU) return 0.5f * v * (1.f + erff(v * 0.70710678118654752f));
+  else if constexpr (ACT == ACT_TANH) return tanhf(v);
+  else return v;
 }
 
 template <typename T> B2_DEV float to_f(T v);
@@ -74,9 +83,19 @@ B2_DEV bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Spin on an mbarrier phase.  A watchdog turns a pipeline deadlock into a
+// reported error (printf + trap -> cudaErrorLaunchFailure) after ~2^34 cycles
+// instead of a hung GPU.
 B2_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
+  if (mbar_try_wait(a, parity)) return;
+  const long long t0 = clock64();
   while (!mbar_try_wait(a, parity)) {
+    if (clock64() - t0 > (1ll << 34)) {
+      printf("b2: mbarrier wait timeout (smem 0x%x parity %u) block %d thread %d\n", a, parity,
+             blockIdx.x, threadIdx.x);
+      __trap();
+    }
   }
 }
 
@@ -91,6 +110,19 @@ B2_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+B2_DEV void tma_store_2d(const CUtensorMap* map, const void* smem_src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+B2_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N> B2_DEV void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N> B2_DEV void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
 B2_DEV void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -98,6 +130,12 @@ B2_DEV void tma_prefetch_desc(const CUtensorMap* map) {
 B2_DEV void cp_async_16(uint32_t smem_dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_dst), "l"(src),
                "r"(src_bytes)
+               : "memory");
+}
+// arrive on `bar` once all prior cp.async of this thread have landed; the
+// arrival counts toward the barrier's expected count (.noinc)
+B2_DEV void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
 B2_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }

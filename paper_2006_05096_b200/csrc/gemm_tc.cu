@@ -13,13 +13,18 @@
 // with N fastest so consecutive CTAs share the same A rows in L2):
 //   warp 0      TMA producer (one elected lane)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-5   epilogue: tcgen05.ld 32 lanes x 32 cols, +bias +res, act,
-//               bf16 pack, 16-byte stores; TMEM double buffered (2 x BN cols)
-//               so tile i's epilogue overlaps tile i+1's mainloop
-//   warps 6-9   (gather mode) A producers, one output pixel (row) per thread
+//   warps 2-5   epilogue: tcgen05.ld (32 lanes x 64 cols per chunk), +bias,
+//               +residual (prefetched one chunk ahead into registers), act,
+//               bf16 pack into a 128B-swizzled staging tile, per-warp TMA
+//               store; TMEM double buffered (2 x BN cols) so tile i's
+//               epilogue overlaps tile i+1's mainloop
+//   warps 6-9   (gather mode) A producers, one output pixel (row) per thread;
+//               completion is signalled with cp.async.mbarrier.arrive so the
+//               producers never wait on their own loads
 //
-// Pipelines: smem full/empty ring (STAGES deep) between producers and the MMA
-// thread; tmem full/empty pair between the MMA thread and the epilogue.
+// Pipelines: smem full/empty ring (a.stages deep, sized on the host from the
+// 227 KB budget) between producers and the MMA thread; tmem full/empty pair
+// between the MMA thread and the epilogue.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -27,32 +32,157 @@ namespace b2 {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;
+constexpr int TC_SMEM_MAX = 232448;           // 227 KB: the opt-in per-CTA maximum
+constexpr int TC_EPI_WARPS = 8;               // two warps per TMEM lane quadrant
+constexpr int TC_EPI_BYTES = TC_EPI_WARPS * 2 * 2048;   // 2 staging tiles of 32 x 64 B each
+constexpr int TC_BAR_BYTES = 512;
 
 template <int BN, bool GATHER>
 struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  static constexpr int THREADS = GATHER ? 320 : 192;
+  static constexpr int MAX_STAGES_RAW =
+      (TC_SMEM_MAX - TC_EPI_BYTES - 1024 - TC_BAR_BYTES) / STAGE_BYTES;
+  static constexpr int MAX_STAGES = MAX_STAGES_RAW > 8 ? 8 : MAX_STAGES_RAW;
+  static constexpr int THREADS = (2 + TC_EPI_WARPS + (GATHER ? 4 : 0)) * 32;
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64
                                    : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM =
+      MAX_STAGES * STAGE_BYTES + TC_EPI_BYTES + 1024 + TC_BAR_BYTES;
 };
+
+B2_DEV void add_bf16x8(float* v, const uint4& u) {
+  const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const float2 f = unpack_bf16x2(w4[h]);
+    v[2 * h] += f.x;
+    v[2 * h + 1] += f.y;
+  }
+}
+
+// TMA-store epilogue of one warp, specialised on the activation so the
+// per-element math is branch-free.
+template <int BN, int ACT>
+B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint64_t* tfull,
+                    uint64_t* tempty, uint32_t tmem_base, int ntiles, int lg, int ew, int eh,
+                    int lane) {
+  const bool has_res = a.res != nullptr;
+  int it = 0;
+  // 32-column chunks split between the two warps of each TMEM lane
+  // quadrant (chunk parity = warp half).  Per chunk: tcgen05.ld.x32, +bias,
+  // +residual (prefetched one chunk ahead), act, bf16 pack into a
+  // 64B-swizzled 32x32 staging tile, per-warp TMA store.
+  uint8_t* obuf = sEpi + ew * 4096;
+  uint32_t oi = 0;
+  const uint32_t swz = (lane >> 1) & 3;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int as = it & 1;
+    const uint32_t aph = (it >> 1) & 1;
+    const int m0 = (t / a.tiles_n) * TC_BM;
+    const int n0 = (t % a.tiles_n) * BN;
+    const int row0 = m0 + lg * 32;
+    const int row = row0 + lane;
+    const bool rvalid = row < a.M;
+    const bf16* rrow = has_res ? a.res + (size_t)(rvalid ? row : 0) * a.ldres + n0 : nullptr;
+    uint4 rnext[4];
+    if (has_res) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        rnext[q] = (rvalid && n0 + eh * 32 + q * 8 < a.N)
+                       ? __ldg(reinterpret_cast<const uint4*>(rrow + eh * 32) + q)
+                       : make_uint4(0, 0, 0, 0);
+    }
+    mbar_wait(&tfull[as], aph);
+    tc_fence_after();
+    const uint32_t taddr = tmem_base + (uint32_t(lg * 32) << 16) + as * BN;
+#pragma unroll 1
+    for (int c = eh * 32; c < BN; c += 64) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(taddr + c, r);
+      uint4 rcur[4];
+      if (has_res) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rcur[q] = rnext[q];
+        if (c + 64 < BN) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            rnext[q] = (rvalid && n0 + c + 64 + q * 8 < a.N)
+                           ? __ldg(reinterpret_cast<const uint4*>(rrow + c + 64) + q)
+                           : make_uint4(0, 0, 0, 0);
+        }
+      }
+      float bv[32];
+      if (a.bias) {
+        const float4* bp = reinterpret_cast<const float4*>(a.bias + n0 + c);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 b4 = __ldg(bp + q);
+          bv[4 * q] = b4.x;
+          bv[4 * q + 1] = b4.y;
+          bv[4 * q + 2] = b4.z;
+          bv[4 * q + 3] = b4.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) bv[j] = 0.f;
+      }
+      tmem_wait_ld();
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + bv[j];
+      if (has_res) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) add_bf16x8(v + 8 * q, rcur[q]);
+      }
+      if (lane == 0 && a.epi_debug != 4 && a.epi_debug != 5) bulk_wait_read<1>();
+      __syncwarp();
+      uint8_t* orow = obuf + (oi & 1) * 2048 + lane * 64;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (a.epi_debug == 6) {
+          if (v[q * 8] == 1234.5f) orow[q] = 1;
+          continue;
+        }
+        uint4 u;
+        u.x = pack_bf16x2(act_t<ACT>(v[q * 8 + 0]), act_t<ACT>(v[q * 8 + 1]));
+        u.y = pack_bf16x2(act_t<ACT>(v[q * 8 + 2]), act_t<ACT>(v[q * 8 + 3]));
+        u.z = pack_bf16x2(act_t<ACT>(v[q * 8 + 4]), act_t<ACT>(v[q * 8 + 5]));
+        u.w = pack_bf16x2(act_t<ACT>(v[q * 8 + 6]), act_t<ACT>(v[q * 8 + 7]));
+        *reinterpret_cast<uint4*>(orow + ((q ^ swz) << 4)) = u;
+      }
+      if (a.epi_debug != 3) fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0 && a.epi_debug != 5) {
+        tma_store_2d(&tmO, obuf + (oi & 1) * 2048, n0 + c, row0);
+        bulk_commit();
+      }
+      ++oi;
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tempty[as]);
+  }
+  if (lane == 0) bulk_wait<0>();
+}
 
 template <int BN, bool GATHER>
 __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                   const __grid_constant__ CUtensorMap tmB, const TcArgs a) {
+                   const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmO,
+                   const __grid_constant__ CUtensorMap tmR,
+                   const __grid_constant__ CUtensorMap tmI, const TcArgs a) {
   using Cfg = TcCfg<BN, GATHER>;
-  constexpr int STAGES = Cfg::STAGES;
+  const int STAGES = a.stages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
+  uint8_t* sEpi = sB + STAGES * Cfg::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + TC_EPI_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -69,13 +199,18 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], TC_EPI_WARPS);
     }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
     if (!GATHER) tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (a.res_kblocks) {
+      tma_prefetch_desc(&tmR);
+      tma_prefetch_desc(&tmI);
+    }
+    if (a.tma_epi) tma_prefetch_desc(&tmO);
   }
   if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
   tc_fence_before();
@@ -91,15 +226,23 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int m0 = (t / a.tiles_n) * TC_BM;
         const int n0 = (t % a.tiles_n) * BN;
-        for (int kb = 0; kb < a.kblocks; ++kb) {
+        for (int kb = 0; kb < a.kblocks + a.res_kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (GATHER) {
-            mbar_arrive_expect_tx(&full[stage], Cfg::B_BYTES);
-          } else {
+          if (kb >= a.kblocks) {
+            // residual fold: A = res[m0:, n0 + j*64:], B = identity rows [0, BN)
+            const int j = kb - a.kblocks;
             mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
-            tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * TC_BK, m0);
+            tma_load_2d(sA + stage * Cfg::A_BYTES, &tmR, &full[stage], n0 + j * TC_BK, m0);
+            tma_load_2d(sB + stage * Cfg::B_BYTES, &tmI, &full[stage], j * TC_BK, 0);
+          } else {
+            if (GATHER) {
+              mbar_arrive_expect_tx(&full[stage], Cfg::B_BYTES);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
+              tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * TC_BK, m0);
+            }
+            tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * TC_BK, n0);
           }
-          tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * TC_BK, n0);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -120,7 +263,7 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
         mbar_wait(&tempty[as], aph ^ 1);
         tc_fence_after();
         const uint32_t dt = tmem_base + as * BN;
-        for (int kb = 0; kb < a.kblocks; ++kb) {
+        for (int kb = 0; kb < a.kblocks + a.res_kblocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = smem_desc_sw128(smem_u32(sA + stage * Cfg::A_BYTES));
@@ -137,93 +280,113 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
         umma_commit(&tfull[as]);
       }
     }
-  } else if (warp < 6) {
+  } else if (warp < 2 + TC_EPI_WARPS) {
     // ------------------------------------------------------------ epilogue
-    const int lg = warp & 3;
+    const int lg = warp & 3;          // TMEM lane quadrant this warp may access
+    const int ew = warp - 2;
+    const int eh = ew >> 2;           // which half of each quadrant's columns
+    const bool has_res = a.res != nullptr;
     int it = 0;
-    const bool vec_ok = (a.ldo % 8 == 0) && (a.res == nullptr || a.ldres % 8 == 0);
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      const int as = it & 1;
-      const uint32_t aph = (it >> 1) & 1;
-      const int m0 = (t / a.tiles_n) * TC_BM;
-      const int n0 = (t % a.tiles_n) * BN;
-      mbar_wait(&tfull[as], aph);
-      tc_fence_after();
-      const int row = m0 + lg * 32 + lane;
-      const uint32_t taddr = tmem_base + (uint32_t(lg * 32) << 16) + as * BN;
-      constexpr int CH = BN >= 32 ? 32 : BN;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += CH) {
-        float v[32];
-        if constexpr (CH == 32) {
+    if (a.epi_debug == 1) {
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int as = it & 1;
+        mbar_wait(&tfull[as], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + (uint32_t(lg * 32) << 16) + as * BN;
+        uint32_t acc = 0;
+        for (int c = eh * 32; c + 32 <= BN; c += 64) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(taddr + c, r);
           tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        } else {
-          uint32_t r[16];
-          tmem_ld_32x32b_x16(taddr + c, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+          acc ^= r[0] ^ r[31];
         }
-        const int col0 = n0 + c;
-        if (row < a.M && col0 < a.N) {
-          if (vec_ok && col0 + CH <= a.N) {
+        if (acc == 0x7f7f7f7fu) a.out[0] = __float2bfloat16_rn(0.f);   // keep the loads alive
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[as]);
+      }
+    } else if (BN >= 32 && a.tma_epi) {
+      switch (a.act) {
+        case ACT_RELU: epi_tma<BN, ACT_RELU>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane); break;
+        case ACT_RELU6: epi_tma<BN, ACT_RELU6>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane); break;
+        case ACT_GELU: epi_tma<BN, ACT_GELU>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane); break;
+        case ACT_TANH: epi_tma<BN, ACT_TANH>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane); break;
+        default: epi_tma<BN, ACT_NONE>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane); break;
+      }
+    } else {
+      // direct path (narrow tiles / N not a multiple of 8): 16-byte stores
+      const bool vec_ok = (a.ldo % 8 == 0) && (!has_res || a.ldres % 8 == 0);
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int as = it & 1;
+        const uint32_t aph = (it >> 1) & 1;
+        const int m0 = (t / a.tiles_n) * TC_BM;
+        const int n0 = (t % a.tiles_n) * BN;
+        mbar_wait(&tfull[as], aph);
+        tc_fence_after();
+        const int row = m0 + lg * 32 + lane;
+        const uint32_t taddr = tmem_base + (uint32_t(lg * 32) << 16) + as * BN;
+        constexpr int CH = BN >= 32 ? 32 : BN;
+#pragma unroll 1
+        for (int c = eh * CH; c < BN; c += 2 * CH) {
+          float v[32];
+          if constexpr (CH == 32) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(taddr + c, r);
+            tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < CH; ++j) {
-              if (a.bias) v[j] += __ldg(a.bias + col0 + j);
-            }
-            if (a.res) {
-              const uint4* rp =
-                  reinterpret_cast<const uint4*>(a.res + (size_t)row * a.ldres + col0);
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          } else {
+            uint32_t r[16];
+            tmem_ld_32x32b_x16(taddr + c, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+          }
+          const int col0 = n0 + c;
+          if (row < a.M && col0 < a.N) {
+            if (vec_ok && col0 + CH <= a.N) {
+#pragma unroll
+              for (int j = 0; j < CH; ++j)
+                if (a.bias) v[j] += __ldg(a.bias + col0 + j);
+              if (has_res) {
+                const uint4* rp =
+                    reinterpret_cast<const uint4*>(a.res + (size_t)row * a.ldres + col0);
+#pragma unroll
+                for (int q = 0; q < CH / 8; ++q) add_bf16x8(v + 8 * q, __ldg(rp + q));
+              }
+              uint4* op = reinterpret_cast<uint4*>(a.out + (size_t)row * a.ldo + col0);
 #pragma unroll
               for (int q = 0; q < CH / 8; ++q) {
-                uint4 u = __ldg(rp + q);
-                uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                  float2 f = unpack_bf16x2(w4[h]);
-                  v[q * 8 + 2 * h] += f.x;
-                  v[q * 8 + 2 * h + 1] += f.y;
-                }
+                uint4 u;
+                u.x = pack_bf16x2(act_apply(v[q * 8 + 0], a.act), act_apply(v[q * 8 + 1], a.act));
+                u.y = pack_bf16x2(act_apply(v[q * 8 + 2], a.act), act_apply(v[q * 8 + 3], a.act));
+                u.z = pack_bf16x2(act_apply(v[q * 8 + 4], a.act), act_apply(v[q * 8 + 5], a.act));
+                u.w = pack_bf16x2(act_apply(v[q * 8 + 6], a.act), act_apply(v[q * 8 + 7], a.act));
+                op[q] = u;
               }
-            }
-            uint4* op = reinterpret_cast<uint4*>(a.out + (size_t)row * a.ldo + col0);
-#pragma unroll
-            for (int q = 0; q < CH / 8; ++q) {
-              uint4 u;
-              u.x = pack_bf16x2(act_apply(v[q * 8 + 0], a.act), act_apply(v[q * 8 + 1], a.act));
-              u.y = pack_bf16x2(act_apply(v[q * 8 + 2], a.act), act_apply(v[q * 8 + 3], a.act));
-              u.z = pack_bf16x2(act_apply(v[q * 8 + 4], a.act), act_apply(v[q * 8 + 5], a.act));
-              u.w = pack_bf16x2(act_apply(v[q * 8 + 6], a.act), act_apply(v[q * 8 + 7], a.act));
-              op[q] = u;
-            }
-          } else {
-            for (int j = 0; j < CH; ++j) {
-              const int col = col0 + j;
-              if (col >= a.N) break;
-              float x = v[j];
-              if (a.bias) x += a.bias[col];
-              if (a.res) x += __bfloat162float(a.res[(size_t)row * a.ldres + col]);
-              a.out[(size_t)row * a.ldo + col] = __float2bfloat16_rn(act_apply(x, a.act));
+            } else {
+              for (int j = 0; j < CH; ++j) {
+                const int col = col0 + j;
+                if (col >= a.N) break;
+                float x = v[j];
+                if (a.bias) x += a.bias[col];
+                if (has_res) x += __bfloat162float(a.res[(size_t)row * a.ldres + col]);
+                a.out[(size_t)row * a.ldo + col] = __float2bfloat16_rn(act_apply(x, a.act));
+              }
             }
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[as]);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[as]);
     }
   } else if (GATHER) {
     // ------------------------------------------------------------ im2col gather
-    constexpr int LAG = 2;
-    const int g = threadIdx.x - 6 * 32;   // row of the A tile owned by this thread
+    const int g = threadIdx.x - (2 + TC_EPI_WARPS) * 32;   // A-tile row owned by this thread
     const uint32_t sw = g & 7;
     int stage = 0;
     uint32_t phase = 0;
-    int issued = 0;
     const size_t img_elems = (size_t)a.H * a.W * a.C;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int m = (t / a.tiles_n) * TC_BM + g;
@@ -241,7 +404,20 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
       for (int kb = 0; kb < a.kblocks; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         const uint32_t dst = smem_u32(sA + stage * Cfg::A_BYTES) + g * 128;
-        if (a.c_div64) {
+        if (a.gmode == 2) {
+          // S*C <= 64: K block kb is filter row r = kb; its S taps are one
+          // contiguous run of S*C channels starting at input column iw0
+          const int ih = ih0 + kb;
+          const bool rok = vrow && (unsigned)ih < (unsigned)a.H;
+          const bf16* rowp = xb + ((long)ih * a.W + iw0) * a.C;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int e = j * 8;
+            const int s = e >> a.c_log2;
+            const bool ok = rok && e < a.SC && (unsigned)(iw0 + s) < (unsigned)a.W;
+            cp_async_16(dst + ((j ^ sw) << 4), ok ? rowp + e : a.x, ok ? 16u : 0u);
+          }
+        } else if (a.gmode == 1) {
           // C % 64 == 0: the whole 64-wide K block is one filter tap
           const int k0 = kb * TC_BK;
           const int tap = k0 / a.C;
@@ -275,15 +451,15 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
             cp_async_16(dst + ((j ^ sw) << 4), src, bytes);
           }
         }
-        cp_async_commit();
-        if (issued >= LAG) {
-          cp_async_wait<LAG>();
-          fence_proxy_async_smem();
-          int ps = stage - LAG;
-          if (ps < 0) ps += STAGES;
-          mbar_arrive(&full[ps]);
+        cp_async_mbar_arrive(&full[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
-        ++issued;
+      }
+      for (int j = 0; j < a.res_kblocks; ++j) {   // residual-fold stages: TMA fills A
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive(&full[stage]);
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
@@ -291,12 +467,6 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
       }
     }
     cp_async_wait<0>();
-    fence_proxy_async_smem();
-    for (int i = (issued < LAG ? issued : LAG); i > 0; --i) {
-      int ps = stage - i;
-      if (ps < 0) ps += STAGES;
-      mbar_arrive(&full[ps]);
-    }
   }
 
   tc_fence_before();
@@ -310,7 +480,8 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
 // ------------------------------------------------------------------ host side
 
 template <int BN, bool G>
-static cudaError_t launch_bn(const TcArgs& a, const CUtensorMap& ta, const CUtensorMap& tb,
+static cudaError_t launch_bn(TcArgs a, const CUtensorMap& ta, const CUtensorMap& tb,
+                             const CUtensorMap& to, const CUtensorMap& tr, const CUtensorMap& ti,
                              int num_sms, cudaStream_t st) {
   using Cfg = TcCfg<BN, G>;
   auto kern = tc_gemm_kernel<BN, G>;
@@ -321,9 +492,10 @@ static cudaError_t launch_bn(const TcArgs& a, const CUtensorMap& ta, const CUten
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  if (a.stages <= 0 || a.stages > Cfg::MAX_STAGES) a.stages = Cfg::MAX_STAGES;
   const int tiles = a.tiles_m * a.tiles_n;
   const int grid = tiles < num_sms ? tiles : num_sms;
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(ta, tb, a);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(ta, tb, to, tr, ti, a);
   return cudaGetLastError();
 }
 
@@ -346,11 +518,12 @@ int tc_pick_bn(long M, int N, int num_sms) {
 }
 
 cudaError_t tc_gemm_launch(const TcArgs& a, int bn, bool gather, const CUtensorMap& ta,
-                           const CUtensorMap& tb, int num_sms, cudaStream_t st) {
+                           const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& tr,
+                           const CUtensorMap& ti, int num_sms, cudaStream_t st) {
 #define B2_TC_CASE(BNV)                                                        \
   case BNV:                                                                    \
-    return gather ? launch_bn<BNV, true>(a, ta, tb, num_sms, st)               \
-                  : launch_bn<BNV, false>(a, ta, tb, num_sms, st);
+    return gather ? launch_bn<BNV, true>(a, ta, tb, to, tr, ti, num_sms, st)   \
+                  : launch_bn<BNV, false>(a, ta, tb, to, tr, ti, num_sms, st);
   switch (bn) {
     B2_TC_CASE(16)
     B2_TC_CASE(32)

@@ -194,9 +194,64 @@ __global__ void dwconv_kernel(const T* __restrict__ x, const T* __restrict__ w,
   }
   y[i] = from_f<T>(act_apply(acc, act));
 }
+// 16-byte vectors of channels: VEC = 8 (bf16) or 4 (fp32) channels per thread
+template <typename T> struct Vec16 {
+  static constexpr int N = 16 / sizeof(T);
+  union {
+    uint4 u;
+    T e[16 / sizeof(T)];
+  };
+};
+
+template <typename T>
+__global__ void dwconv_vec_kernel(const T* __restrict__ x, const T* __restrict__ w,
+                                  const float* __restrict__ bias, T* __restrict__ y, int B,
+                                  int H, int W, int C, int R, int stride, int pad, int OH, int OW,
+                                  int act) {
+  constexpr int V = Vec16<T>::N;
+  const int CV = C / V;
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long total = (long)B * OH * OW * CV;
+  if (i >= total) return;
+  const int cv = (int)(i % CV);
+  long p = i / CV;
+  const int ow = (int)(p % OW);
+  p /= OW;
+  const int oh = (int)(p % OH);
+  const long b = p / OH;
+  const int c0 = cv * V;
+  float acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = bias ? bias[c0 + k] : 0.f;
+  const int ih0 = oh * stride - pad, iw0 = ow * stride - pad;
+  for (int r = 0; r < R; ++r) {
+    const int ih = ih0 + r;
+    if ((unsigned)ih >= (unsigned)H) continue;
+    for (int s = 0; s < R; ++s) {
+      const int iw = iw0 + s;
+      if ((unsigned)iw >= (unsigned)W) continue;
+      Vec16<T> xv, wv;
+      xv.u = __ldg(reinterpret_cast<const uint4*>(x + ((b * H + ih) * W + iw) * C + c0));
+      wv.u = __ldg(reinterpret_cast<const uint4*>(w + (r * R + s) * C + c0));
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] = fmaf(to_f(xv.e[k]), to_f(wv.e[k]), acc[k]);
+    }
+  }
+  Vec16<T> ov;
+#pragma unroll
+  for (int k = 0; k < V; ++k) ov.e[k] = from_f<T>(act_apply(acc[k], act));
+  *reinterpret_cast<uint4*>(y + ((b * OH + oh) * OW + ow) * (long)C + c0) = ov.u;
+}
+
 template <typename T>
 cudaError_t dwconv(const T* x, const T* w, const float* bias, T* y, int B, int H, int W, int C,
                    int R, int stride, int pad, int OH, int OW, int act, cudaStream_t st) {
+  if (C % Vec16<T>::N == 0) {
+    const long total = (long)B * OH * OW * (C / Vec16<T>::N);
+    dwconv_vec_kernel<T><<<nblk(total, 256), 256, 0, st>>>(x, w, bias, y, B, H, W, C, R, stride,
+                                                           pad, OH, OW, act);
+    return cudaGetLastError();
+  }
   const long total = (long)B * OH * OW * C;
   dwconv_kernel<T><<<nblk(total, 256), 256, 0, st>>>(x, w, bias, y, B, H, W, C, R, stride, pad,
                                                      OH, OW, act);
@@ -229,8 +284,49 @@ __global__ void maxpool_kernel(const T* __restrict__ x, T* __restrict__ y, int B
   y[i] = from_f<T>(m);
 }
 template <typename T>
+__global__ void maxpool_vec_kernel(const T* __restrict__ x, T* __restrict__ y, int B, int H,
+                                   int W, int C, int k, int stride, int pad, int OH, int OW) {
+  constexpr int V = Vec16<T>::N;
+  const int CV = C / V;
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long total = (long)B * OH * OW * CV;
+  if (i >= total) return;
+  const int cv = (int)(i % CV);
+  long p = i / CV;
+  const int ow = (int)(p % OW);
+  p /= OW;
+  const int oh = (int)(p % OH);
+  const long b = p / OH;
+  float m[V];
+#pragma unroll
+  for (int q = 0; q < V; ++q) m[q] = -INFINITY;
+  for (int r = 0; r < k; ++r) {
+    const int ih = oh * stride - pad + r;
+    if ((unsigned)ih >= (unsigned)H) continue;
+    for (int s = 0; s < k; ++s) {
+      const int iw = ow * stride - pad + s;
+      if ((unsigned)iw >= (unsigned)W) continue;
+      Vec16<T> v;
+      v.u = __ldg(reinterpret_cast<const uint4*>(x + ((b * H + ih) * W + iw) * C + cv * V));
+#pragma unroll
+      for (int q = 0; q < V; ++q) m[q] = fmaxf(m[q], to_f(v.e[q]));
+    }
+  }
+  Vec16<T> o;
+#pragma unroll
+  for (int q = 0; q < V; ++q) o.e[q] = from_f<T>(m[q]);
+  reinterpret_cast<uint4*>(y)[i] = o.u;
+}
+
+template <typename T>
 cudaError_t maxpool(const T* x, T* y, int B, int H, int W, int C, int k, int stride, int pad,
                     int OH, int OW, cudaStream_t st) {
+  if (C % Vec16<T>::N == 0) {
+    const long tv = (long)B * OH * OW * (C / Vec16<T>::N);
+    maxpool_vec_kernel<T><<<nblk(tv, 256), 256, 0, st>>>(x, y, B, H, W, C, k, stride, pad, OH,
+                                                         OW);
+    return cudaGetLastError();
+  }
   const long total = (long)B * OH * OW * C;
   maxpool_kernel<T><<<nblk(total, 256), 256, 0, st>>>(x, y, B, H, W, C, k, stride, pad, OH, OW);
   return cudaGetLastError();

@@ -24,12 +24,23 @@ struct TcArgs {
   // gather (implicit im2col) parameters, NHWC input
   const bf16* x;
   int H, W, C, OW, OHW, S, stride, pad;
-  int c_div64;          // C % 64 == 0 -> one filter tap per K block
+  int gmode;            // 1: C % 64 == 0 (one filter tap per K block)
+                        // 2: S*C <= 64, C = 2^c_log2 (one filter row per K block)
+                        // 3: generic (per-chunk tap decomposition)
+  int c_log2, SC;
+  int tma_epi;          // epilogue through smem + TMA store (N % 8 == 0, BN >= 64)
+  int stages;           // smem pipeline depth (0 = the most that fits)
+  int epi_debug;        // 0 normal; 1 drain TMEM only (no math/stores) — profiling aid
+  int res_kblocks;      // >0: residual folded into the MMA as [A | res] x [W | I]^T;
+                        // BN/64 extra K blocks per tile, A from tmR, B from the identity
 };
 
 int tc_pick_bn(long M, int N, int num_sms);
 cudaError_t tc_gemm_launch(const TcArgs& a, int bn, bool gather, const CUtensorMap& ta,
-                           const CUtensorMap& tb, int num_sms, cudaStream_t st);
+                           const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& tr,
+                           const CUtensorMap& ti, int num_sms, cudaStream_t st);
+
+cudaError_t attention_tc(const CUtensorMap& tm_qkv, bf16* out, int B, int H, cudaStream_t st);
 
 // ---- SIMT kernels (templated on storage type: float or bf16) -----------------
 struct GemmSimtArgs {

@@ -110,16 +110,17 @@ EncodeTiledFn encode_fn() {
 // bf16 matrix [rows, cols] with a row pitch in bytes; box = 64 cols x box_rows,
 // 128-byte swizzle (the canonical UMMA K-major layout)
 bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
-                    uint64_t row_bytes, uint32_t box_rows) {
+                    uint64_t row_bytes, uint32_t box_rows, uint32_t box_cols = 64,
+                    CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {row_bytes};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t es[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
-            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // ------------------------------------------------------------------ executor state
@@ -135,6 +136,7 @@ struct Layer {
   void* w3 = nullptr;       // embed: type row (T)
   // GEMM execution choices
   bool tc = false, gather = false;
+  int gmode = 0;            // see TcArgs::gmode
   int K = 0, kpad = 0, ldw = 0;
 };
 
@@ -146,6 +148,10 @@ struct BatchState {
   std::vector<int> bn;             // per layer (tc)
   std::vector<CUtensorMap> tmA;    // per layer (tc, TMA mode)
   std::vector<CUtensorMap> tmB;    // per layer (tc): weights, box rows = BN
+  std::vector<CUtensorMap> tmO;    // per layer (tc): output, 32x32 box, 64B swizzle
+  std::vector<CUtensorMap> tmR;    // per layer (tc, residual fold): residual as an A operand
+  std::vector<char> fold;          // per layer: residual folded into the MMA
+  std::vector<CUtensorMap> tmI;    // per layer: identity [256 x 256] (box rows = BN) for the fold
   cudaGraphExec_t graph = nullptr;
   void* h_in = nullptr;            // pinned (e2e)
   void* h_out = nullptr;
@@ -170,6 +176,10 @@ struct b2_plan {
   size_t flush_bytes = 0;
   bool force_simt = false;
   int launches = 0;
+  int epi_mode = 0;          // B2_EPI_MODE: 0 TMA-store epilogue, 1 drain-only, 2 direct stores
+  int fold_max_k = 256;      // B2_FOLD_MAX_K: fold residuals into the MMA when K <= this
+  void* identity = nullptr;  // bf16 I[256][256]
+  int stages_override = 0;   // B2_STAGES
 };
 
 namespace {
@@ -178,7 +188,9 @@ template <typename T> size_t tsize() { return sizeof(T); }
 
 int upload_f32(b2_plan* pl, const float* src, size_t n, float** out) {
   float* d = nullptr;
-  CK(cudaMalloc(&d, n * sizeof(float) + 16));
+  const size_t padded = (n + 255) / 256 * 256;   // epilogues read whole 32-column chunks
+  CK(cudaMalloc(&d, padded * sizeof(float)));
+  CK(cudaMemset(d, 0, padded * sizeof(float)));
   pl->allocs.push_back(d);
   CK(cudaMemcpy(d, src, n * sizeof(float), cudaMemcpyHostToDevice));
   pl->weight_bytes += n * sizeof(float);
@@ -236,11 +248,21 @@ int upload_weights(b2_plan* pl, const uint8_t* data, const std::vector<WeightRec
             return fail(B2_ERR_UNSUPPORTED, "bf16 %s needs channels %% 8 == 0 (got %d)",
                         conv ? "conv" : "linear", C);
           L.gather = !plain;
-          L.kpad = (K + 63) / 64 * 64;
+          const int R = conv ? L.p[8] : 1, S = conv ? L.p[9] : 1;
+          const bool pow2 = (C & (C - 1)) == 0;
+          L.gmode = !L.gather ? 0 : (C % 64 == 0) ? 1 : (S * C <= 64 && pow2) ? 2 : 3;
+          L.kpad = L.gmode == 2 ? R * 64 : (K + 63) / 64 * 64;
           L.ldw = L.kpad;
           std::vector<float> h((size_t)N * L.kpad, 0.f);
-          for (int r = 0; r < N; ++r)
-            memcpy(&h[(size_t)r * L.kpad], w + (size_t)r * K, sizeof(float) * K);
+          if (L.gmode == 2) {   // [N][R][64]: each filter row's (s, c) run padded to 64
+            for (int n = 0; n < N; ++n)
+              for (int r = 0; r < R; ++r)
+                memcpy(&h[(size_t)n * L.kpad + r * 64], w + (size_t)n * K + (size_t)r * S * C,
+                       sizeof(float) * S * C);
+          } else {
+            for (int r = 0; r < N; ++r)
+              memcpy(&h[(size_t)r * L.kpad], w + (size_t)r * K, sizeof(float) * K);
+          }
           if ((rc = upload_as<bf16>(pl, h, &L.w))) return rc;
         } else {
           L.ldw = K;
@@ -299,6 +321,9 @@ int upload_weights(b2_plan* pl, const uint8_t* data, const std::vector<WeightRec
         if ((rc = upload_f32(pl, g, n4, &L.g)) || (rc = upload_f32(pl, b, n5, &L.b))) return rc;
         break;
       }
+      case OP_ATTENTION:
+        L.tc = bf && !pl->force_simt && L.p[4] == 128 && L.p[3] == 64;
+        break;
       default:
         break;
     }
@@ -375,7 +400,8 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
           a.kblocks = L.kpad / 64;
           a.Kreal = L.K;
           a.bias = L.bias;
-          a.res = res_t >= 0 ? reinterpret_cast<const bf16*>(S.act[res_t]) : nullptr;
+          a.res = (res_t >= 0 && !S.fold[li]) ? reinterpret_cast<const bf16*>(S.act[res_t])
+                                              : nullptr;
           a.ldres = N;
           a.out = reinterpret_cast<bf16*>(out);
           a.ldo = N;
@@ -393,10 +419,19 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
             a.S = p[9];
             a.stride = p[10];
             a.pad = p[11];
-            a.c_div64 = (p[6] % 64) == 0;
+            a.gmode = L.gmode;
+            int lg2 = 0;
+            while ((1 << lg2) < p[6]) ++lg2;
+            a.c_log2 = lg2;
+            a.SC = p[9] * p[6];
           }
+          a.tma_epi = bn >= 32 && N % 8 == 0 && pl->epi_mode != 2;
+          a.epi_debug = pl->epi_mode == 2 ? 0 : pl->epi_mode;
+          a.stages = pl->stages_override;
+          a.res_kblocks = S.fold[li] ? bn / 64 : 0;
           CK(tc_gemm_launch(a, bn, L.gather, L.gather ? S.tmB[li] : S.tmA[li], S.tmB[li],
-                            pl->num_sms, st));
+                            S.tmO[li], S.fold[li] ? S.tmR[li] : S.tmO[li],
+                            S.fold[li] ? S.tmI[li] : S.tmO[li], pl->num_sms, st));
         } else {
           GemmSimtArgs a{};
           a.M = (int)M;
@@ -458,7 +493,10 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
         break;
       }
       case OP_ATTENTION:
-        CK(attention<T>(A(p[0]), A(p[1]), B, p[4], p[2], p[3], st));
+        if (L.tc)
+          CK(attention_tc(S.tmA[li], reinterpret_cast<bf16*>(S.act[p[1]]), B, p[2], st));
+        else
+          CK(attention<T>(A(p[0]), A(p[1]), B, p[4], p[2], p[3], st));
         ++launches;
         break;
       case OP_ACT:
@@ -509,10 +547,20 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
   S.bn.assign(pl->layers.size(), 0);
   S.tmA.resize(pl->layers.size());
   S.tmB.resize(pl->layers.size());
+  S.tmO.resize(pl->layers.size());
+  S.tmR.resize(pl->layers.size());
+  S.fold.assign(pl->layers.size(), 0);
+  S.tmI.resize(pl->layers.size());
   for (size_t li = 0; li < pl->layers.size(); ++li) {
     Layer& L = pl->layers[li];
     if (!L.tc) continue;
     const int* p = L.p;
+    if (L.kind == OP_ATTENTION) {
+      const uint64_t cols = 3ull * p[2] * p[3];
+      if (!make_tmap_bf16(&S.tmA[li], S.act[p[0]], (uint64_t)batch * p[4], cols, cols * 2, 128))
+        return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeTiled(qkv) failed", li);
+      continue;
+    }
     const bool conv = L.kind == OP_CONV;
     const int N = conv ? p[7] : p[5];
     const long M = conv ? (long)batch * p[12] * p[13] : (long)batch * p[6];
@@ -521,6 +569,21 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     if (!make_tmap_bf16(&S.tmB[li], L.w, (uint64_t)N, (uint64_t)L.kpad, (uint64_t)L.kpad * 2,
                         (uint32_t)bn))
       return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeTiled(B) failed", li);
+    if (bn >= 32 && N % 8 == 0) {
+      if (!make_tmap_bf16(&S.tmO[li], S.act[p[1]], (uint64_t)M, (uint64_t)N, (uint64_t)N * 2, 32,
+                          32, CU_TENSOR_MAP_SWIZZLE_64B))
+        return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeTiled(out) failed", li);
+    }
+    // residual fold: cheap in MMA time when K is small, and it moves the
+    // residual read out of the epilogue into the TMA pipeline
+    const int res_t = conv ? p[15] : p[8];
+    if (res_t >= 0 && bn >= 64 && N % 8 == 0 && L.K <= pl->fold_max_k && pl->identity) {
+      if (!make_tmap_bf16(&S.tmR[li], S.act[res_t], (uint64_t)M, (uint64_t)N, (uint64_t)N * 2,
+                          128) ||
+          !make_tmap_bf16(&S.tmI[li], pl->identity, 256, 256, 512, (uint32_t)bn))
+        return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeTiled(res/identity) failed", li);
+      S.fold[li] = 1;
+    }
     if (!L.gather) {
       const int K = L.K;
       const long ld = conv ? p[6] : p[9];
@@ -614,6 +677,9 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   pl->out_elems = h.out_elems;
   const char* fs = getenv("B2_FORCE_SIMT");
   pl->force_simt = fs && fs[0] == '1';
+  if (const char* em = getenv("B2_EPI_MODE")) pl->epi_mode = atoi(em);
+  if (const char* sg = getenv("B2_STAGES")) pl->stages_override = atoi(sg);
+  if (const char* fk = getenv("B2_FOLD_MAX_K")) pl->fold_max_k = atoi(fk);
   cudaGetDevice(&pl->device);
   cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, pl->device);
   int major = 0;
@@ -645,6 +711,11 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   }
   int rc = validate_ops(pl);
   if (!rc) rc = upload_weights(pl, d + pos, wr, len - 4 - pos);
+  if (!rc && pl->dtype == B2_DT_BF16) {
+    std::vector<float> eye(256 * 256, 0.f);
+    for (int i = 0; i < 256; ++i) eye[i * 256 + i] = 1.f;
+    rc = upload_as<bf16>(pl, eye, &pl->identity);
+  }
   if (!rc) {
     // algorithmic FLOPs (2 per MAC) of the contraction ops
     for (const Layer& L : pl->layers) {
@@ -806,6 +877,20 @@ int b2_profile_ops(b2_plan* pl, int batch, int iters, float* op_ms, int* n_ops, 
   }
   *n_ops = (int)nl;
   for (auto& e : ev) cudaEventDestroy(e);
+  return B2_OK;
+}
+
+int b2_read_tensor(b2_plan* pl, int batch, int tensor, void* host_out, size_t bytes) {
+  if (!pl || !host_out) return fail(B2_ERR_ARG, "null argument");
+  if (tensor < 0 || tensor >= (int)pl->tensors.size()) return fail(B2_ERR_ARG, "bad tensor id");
+  auto it = pl->states.find(batch);
+  if (it == pl->states.end()) return fail(B2_ERR_ARG, "no forward has run at batch %d", batch);
+  const size_t need = (size_t)batch * pl->tensors[tensor].elems * elem_size(pl, tensor);
+  if (bytes < need) return fail(B2_ERR_ARG, "buffer too small (%zu < %zu)", bytes, need);
+  int rc = check_device(pl);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(pl->stream));
+  CK(cudaMemcpy(host_out, it->second.act[tensor], need, cudaMemcpyDeviceToHost));
   return B2_OK;
 }
 

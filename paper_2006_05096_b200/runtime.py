@@ -46,6 +46,7 @@ def _declare(lib):
         "b2_gen_input": (c.c_int, [P, P, c.c_int, c.c_uint64, P]),
         "b2_profile_ops": (c.c_int, [P, c.c_int, c.c_int, c.POINTER(c.c_float),
                                      c.POINTER(c.c_int), c.POINTER(c.c_int)]),
+        "b2_read_tensor": (c.c_int, [P, c.c_int, c.c_int, P, c.c_size_t]),
         "b2_plan_destroy": (None, [P]),
         "b2_last_error": (c.c_char_p, []),
         "b2_version": (c.c_char_p, []),
@@ -58,7 +59,8 @@ def _declare(lib):
 
 
 EXPORTED = ("b2_plan_create", "b2_plan_io", "b2_plan_info", "b2_forward", "b2_forward_host",
-            "b2_bench", "b2_bench_e2e", "b2_gen_input", "b2_profile_ops", "b2_plan_destroy",
+            "b2_bench", "b2_bench_e2e", "b2_gen_input", "b2_profile_ops", "b2_read_tensor",
+            "b2_plan_destroy",
             "b2_last_error", "b2_version")
 
 
@@ -167,6 +169,22 @@ class Plan:
         if rc != B2_OK:
             _raise(rc, "bench")
         return lat, comp
+
+    def read_tensor(self, batch: int, tensor: int, elems: int, kind: int) -> np.ndarray:
+        """Activation `tensor` of the last forward at `batch`, as float64 (or
+        int32 ids) — the verification hook used by the layerwise parity tests."""
+        if kind == 1:
+            buf = np.empty(batch * elems, dtype=np.int32)
+        elif self.dtype == DT_BF16:
+            buf = np.empty(batch * elems, dtype=np.uint16)
+        else:
+            buf = np.empty(batch * elems, dtype=np.float32)
+        rc = self._lib.b2_read_tensor(self._h, batch, tensor, buf.ctypes.data, buf.nbytes)
+        if rc != B2_OK:
+            _raise(rc, "read_tensor")
+        if buf.dtype == np.uint16:
+            return (buf.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        return buf.astype(np.float64) if kind != 1 else buf
 
     def profile_ops(self, batch: int, iters: int = 5) -> list[tuple[int, float]]:
         cap = 4096

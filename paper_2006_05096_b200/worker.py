@@ -1,0 +1,252 @@
+"""The B200 executor process: ``python -m paper_2006_05096_b200.worker``.
+
+Drop-in for the reference's serving backend (pkg/src/modelci/mockserve/
+__main__.py:18-60, server.py:91-241) behind the same process contract:
+
+* ``--model PATH --protocol rest|grpc-style``; prints ``READY <port>`` once
+  listening; exits 2 when the model does not decode (b200-plan, or a toy
+  graph which is converted on load); exits 3 when no usable GPU is visible
+  (there is no CPU fallback); dies on SIGTERM.
+* rest: ``GET /health``; ``POST /predict {"inputs": [[...]]}`` ->
+  ``{"outputs", "batch", "service_ms"}`` (400 on an empty batch);
+  ``POST /bench`` and ``POST /info`` (new).  TCP_NODELAY is set, removing the
+  reference's ~44 ms Nagle floor.
+* grpc-style: 4-byte big-endian framed JSON ``{"kind": "health"|"predict"}``
+  plus ``predict_bin`` / ``bench`` / ``info`` (wire.py).
+
+``predict`` runs the real forward (libb2 ``b2_forward_host``) instead of
+sleeping; ``service_ms`` is the measured device-side request time.  ``bench``
+runs a sweep cell's closed loop on the device (libb2 ``b2_bench``).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import signal
+import socketserver
+import sys
+import threading
+import time
+from http.server import BaseHTTPRequestHandler, ThreadingHTTPServer
+from pathlib import Path
+
+import numpy as np
+
+from . import plan as P
+from . import toyformat, wire, zoo
+from .errors import LaunchFailure, ModelCIError, PlanFormatError, ToyFormatError
+
+FORMAT_EXIT = 2
+NO_DEVICE_EXIT = 3
+
+
+def load_plan_bytes(data: bytes) -> bytes:
+    """b200-plan bytes from a variant file (plans pass through; toy graphs are
+    lowered with the toy converter, so a reference toy variant also loads)."""
+    if data[:4] == P.MAGIC:
+        P.decode(data)   # validate: magic, CRC, tables
+        return data
+    graph = toyformat.load_model(data)
+    return zoo.emit_toy(graph, "toy").build(P.DT_FP32)
+
+
+class Executor:
+    """Model behaviour shared by both protocols (the MockServer analogue)."""
+
+    def __init__(self, plan_bytes: bytes, dtype: int):
+        from .runtime import Plan
+        self.plan = Plan(plan_bytes, dtype)
+        self.meta = P.decode(plan_bytes).meta
+        self.started = time.monotonic()
+
+    def healthy(self) -> bool:
+        return True
+
+    def info(self) -> dict:
+        p = self.plan
+        return {"ok": True, "in_elems": p.in_elems, "out_elems": p.out_elems,
+                "in_kind": p.in_kind, "dtype": p.dtype, "flops_per_sample": p.flops_per_sample,
+                "weight_bytes": p.weight_bytes, "launches_per_forward": p.launches_per_forward,
+                "model": self.meta.get("model", "")}
+
+    def predict_array(self, x: np.ndarray) -> tuple[np.ndarray, float]:
+        t0 = time.perf_counter()
+        out = self.plan.predict(x)
+        return out, (time.perf_counter() - t0) * 1000.0
+
+    def predict(self, inputs) -> dict:
+        if not isinstance(inputs, list) or not inputs:
+            raise ValueError("batch must be a non-empty list of samples")
+        x = np.asarray(inputs, dtype=self.plan.in_dtype)
+        if x.ndim != 2 or x.shape[1] != self.plan.in_elems:
+            raise ValueError(f"samples must have {self.plan.in_elems} elements")
+        out, ms = self.predict_array(x)
+        return {"outputs": out.tolist(), "batch": int(x.shape[0]), "service_ms": ms}
+
+    def bench(self, req: dict) -> dict:
+        batch = int(req.get("batch", 1))
+        n = int(req.get("n", 100))
+        warm = int(req.get("warmup", 10))
+        seed = int(req.get("seed", 0))
+        if batch < 1 or n < 1:
+            raise ValueError("batch and n must be >= 1")
+        lat, comp = self.plan.bench(batch, n, warm, seed, e2e=bool(req.get("e2e", False)))
+        return {"ok": True, "batch": batch, "latencies_ms": lat.tolist(),
+                "completions_ms": comp.tolist()}
+
+
+class _RestServer(ThreadingHTTPServer):
+    daemon_threads = True
+    allow_reuse_address = True
+
+    def __init__(self, addr, handler, ex: Executor):
+        super().__init__(addr, handler)
+        self.ex = ex
+
+
+class _RestHandler(BaseHTTPRequestHandler):
+    protocol_version = "HTTP/1.1"
+    disable_nagle_algorithm = True
+
+    def log_message(self, fmt, *args):
+        pass
+
+    def _send(self, status: int, payload: dict):
+        body = json.dumps(payload).encode()
+        self.send_response(status)
+        self.send_header("Content-Type", "application/json")
+        self.send_header("Content-Length", str(len(body)))
+        self.end_headers()
+        self.wfile.write(body)
+
+    def do_GET(self):
+        if self.path == "/health":
+            self._send(200, {"status": "ok"})
+        else:
+            self._send(404, {"error": "not found"})
+
+    def do_POST(self):
+        try:
+            n = int(self.headers.get("Content-Length", "0"))
+            req = json.loads(self.rfile.read(n) or b"{}")
+            ex = self.server.ex
+            if self.path == "/predict":
+                self._send(200, ex.predict(req.get("inputs")))
+            elif self.path == "/bench":
+                self._send(200, ex.bench(req))
+            elif self.path == "/info":
+                self._send(200, ex.info())
+            else:
+                self._send(404, {"error": "not found"})
+        except (ValueError, json.JSONDecodeError, ModelCIError) as exc:
+            self._send(400, {"ok": False, "error": str(exc)})
+
+
+class _FrameServer(socketserver.ThreadingTCPServer):
+    daemon_threads = True
+    allow_reuse_address = True
+
+    def __init__(self, addr, handler, ex: Executor):
+        super().__init__(addr, handler)
+        self.ex = ex
+
+
+class _FrameHandler(socketserver.BaseRequestHandler):
+    def handle(self):
+        ex = self.server.ex
+        wire.nodelay(self.request)
+        while True:
+            try:
+                raw = wire.read_frame(self.request)
+            except (ConnectionError, ValueError, OSError):
+                return
+            if raw is None:
+                return
+            try:
+                reply = self._dispatch(ex, raw)
+            except (ValueError, json.JSONDecodeError, ModelCIError) as exc:
+                reply = json.dumps({"ok": False, "error": str(exc)}).encode()
+            try:
+                wire.write_frame(self.request, reply)
+            except (ConnectionError, OSError):
+                return
+
+    @staticmethod
+    def _dispatch(ex: Executor, raw: bytes) -> bytes:
+        if raw.startswith(wire.BIN_MAGIC):
+            head, body = wire.unpack_bin(raw)
+            if head.get("kind") != "predict_bin":
+                raise ValueError(f"unknown binary kind '{head.get('kind')}'")
+            batch = int(head.get("batch", 0))
+            x = np.frombuffer(body, dtype=ex.plan.in_dtype)
+            if batch < 1 or x.size != batch * ex.plan.in_elems:
+                raise ValueError("binary batch does not match the model input size")
+            out, ms = ex.predict_array(x.reshape(batch, ex.plan.in_elems))
+            return wire.pack_bin({"ok": True, "batch": batch, "out_elems": ex.plan.out_elems,
+                                  "service_ms": ms}, out.tobytes())
+        msg = json.loads(raw)
+        kind = msg.get("kind")
+        if kind == "health":
+            reply = {"ok": True, "status": "ok"}
+        elif kind == "predict":
+            reply = dict(ex.predict(msg.get("inputs")), ok=True)
+        elif kind == "bench":
+            reply = ex.bench(msg)
+        elif kind == "info":
+            reply = ex.info()
+        else:
+            reply = {"ok": False, "error": f"unknown kind '{kind}'"}
+        return json.dumps(reply).encode()
+
+
+def serve(ex: Executor, protocol: str, host: str = "127.0.0.1"):
+    if protocol == "rest":
+        return _RestServer((host, 0), _RestHandler, ex)
+    if protocol == "grpc-style":
+        return _FrameServer((host, 0), _FrameHandler, ex)
+    raise ValueError(f"unknown protocol '{protocol}'")
+
+
+def build_parser() -> argparse.ArgumentParser:
+    ap = argparse.ArgumentParser(prog="b200-worker", description="B200 model executor")
+    ap.add_argument("--model", required=True)
+    ap.add_argument("--protocol", choices=["rest", "grpc-style"], default="rest")
+    ap.add_argument("--host", default="127.0.0.1")
+    ap.add_argument("--dtype", choices=["auto", "bf16", "fp32"], default="auto",
+                    help="execution dtype (auto: the plan header's)")
+    return ap
+
+
+def main(argv=None) -> int:
+    args = build_parser().parse_args(argv)
+    try:
+        data = Path(args.model).read_bytes()
+        plan_bytes = load_plan_bytes(data)
+    except OSError as exc:
+        print(f"cannot read model: {exc}", file=sys.stderr)
+        return FORMAT_EXIT
+    except (PlanFormatError, ToyFormatError) as exc:
+        print(f"cannot decode model: {exc}", file=sys.stderr)
+        return FORMAT_EXIT
+    dtype = {"auto": -1, "bf16": P.DT_BF16, "fp32": P.DT_FP32}[args.dtype]
+    try:
+        ex = Executor(plan_bytes, dtype)
+    except PlanFormatError as exc:
+        print(f"cannot load plan: {exc}", file=sys.stderr)
+        return FORMAT_EXIT
+    except LaunchFailure as exc:
+        print(f"no usable device: {exc}", file=sys.stderr)
+        return NO_DEVICE_EXIT
+    server = serve(ex, args.protocol, args.host)
+    signal.signal(signal.SIGTERM, lambda *_: sys.exit(0))
+    print(f"READY {server.server_address[1]}", flush=True)
+    try:
+        server.serve_forever(poll_interval=0.05)
+    except KeyboardInterrupt:
+        pass
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
