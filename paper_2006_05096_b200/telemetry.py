@@ -170,6 +170,8 @@ class NvmlProvider(DeviceProvider):
             pass
         if util is None:   # per-process accounting unavailable: device-wide figure
             util = self._nv.nvmlDeviceGetUtilizationRates(h).gpu / 100.0
+        if mem == 0:       # pid not visible (PID namespace): device-wide memory in use
+            mem = int(self._nv.nvmlDeviceGetMemoryInfo(h).used)
         return min(max(util, 0.0), 1.0), mem
 
 

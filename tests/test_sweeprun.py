@@ -1,0 +1,104 @@
+"""Multi-device sweep glue: controller-driven per-device concurrency with pool
+cells and LPT, and the static process-per-GPU sharding over a gloo
+world_size-2 group (the N>1 path, CPU only)."""
+import os
+import time
+
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2006_05096_b200.profiler.types import Cell, ProfilingJob, ProfilingResult, SweepSpec
+from paper_2006_05096_b200.sweeprun import (ControllerSweep, cell_cost, gather_results,
+                                            lpt_partition, shard_for_rank)
+
+MODELS = {"mlp": 4.1e5, "mobilenet_v2": 6.0e8, "resnet50": 8.2e9, "bert": 2.2e10,
+          "vgg16": 3.1e10}
+BATCHES = [1, 2, 4, 8, 16, 32, 64, 128, 256]
+
+
+def c4_jobs():
+    return [ProfilingJob(m, "r" + m, "v" + m,
+                         SweepSpec(batch_sizes=BATCHES, devices=["gpu:*"], backends=["b200"],
+                                   protocols=["grpc-style"], requests_per_cell=10,
+                                   warmup_requests=0)) for m in MODELS]
+
+
+def fake_result(job, cell, dev):
+    return ProfilingResult(job.variant_id, dev, cell.backend, cell.protocol, cell.batch_size,
+                           1.0, 1.0, 1.0, 1.0, None, None)
+
+
+def test_controller_sweep_spreads_pool_cells_over_devices():
+    devices = [f"gpu:{i}" for i in range(4)]
+    seen = []
+
+    def run_cell(job, cell, dev):
+        seen.append((job.id, cell.batch_size, dev))
+        time.sleep(0.002 * cell.batch_size / 64)
+        return fake_result(job, cell, dev)
+
+    cost = lambda job, cell: MODELS[job.id] * cell.batch_size
+    sweep = ControllerSweep(devices, run_cell, cost_fn=cost)
+    jobs = c4_jobs()
+    sweep.run(jobs, timeout_s=60)
+    assert all(j.is_done() for j in jobs) and not sweep.errors
+    assert len(seen) == 45 and len({(j, b) for j, b, _ in seen}) == 45
+    assert {d for _, _, d in seen} == set(devices)
+    # LPT: the costliest cell (vgg16 @ 256) is granted first
+    assert sweep.placements[0][0] == "gpu:*|b200|grpc-style|256"
+    assert all(r.device.startswith("gpu:") and r.device != "gpu:*" for j in jobs for r in j.results)
+
+
+def test_controller_sweep_skips_busy_device():
+    devices = ["gpu:0", "gpu:1"]
+    used = set()
+
+    def run_cell(job, cell, dev):
+        used.add(dev)
+        return fake_result(job, cell, dev)
+
+    sweep = ControllerSweep(devices, run_cell, sample=lambda: {"gpu:0": 0.9, "gpu:1": 0.0},
+                            cost_fn=lambda j, c: c.batch_size)
+    jobs = c4_jobs()[:1]
+    sweep.run(jobs, timeout_s=30)
+    assert used == {"gpu:1"}                     # the busy (serving) GPU is never used
+
+
+def test_lpt_partition_balances():
+    units = [(m, b) for m in MODELS for b in BATCHES]
+    cost = lambda u: cell_cost(MODELS[u[0]], Cell("gpu:*", "b200", "grpc-style", u[1]), 100, 10)
+    for k in (2, 4, 8):
+        bins = lpt_partition(units, cost, k)
+        loads = [sum(cost(u) for u in b) for b in bins]
+        assert sorted(u for b in bins for u in b) == sorted(units)
+        assert max(loads) <= sum(loads) / k + max(cost(u) for u in units) + 1e-9
+
+
+def _rank_main(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    units = [(m, b) for m in MODELS for b in BATCHES]
+    cost = lambda u: MODELS[u[0]] * u[1]
+    mine = shard_for_rank(units, cost, rank, world)
+    results = [ProfilingResult("v" + m, f"gpu:{rank}", "b200", "grpc-style", b, 1.0, 1.0, 1.0,
+                               1.0, None, None) for m, b in mine]
+    allres = gather_results(results, rank, world)
+    if rank == 0:
+        q.put([(r.variant_id, r.batch_size, r.device) for r in allres])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_sweep_gloo_world_size_2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+    assert len(got) == 45 and len({(v, b) for v, b, _ in got}) == 45
+    assert {d for _, _, d in got} == {"gpu:0", "gpu:1"}
