@@ -223,9 +223,18 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      const int cpb = a.C >> 6;   // im2col: 64-channel K blocks per filter tap
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int m0 = (t / a.tiles_n) * TC_BM;
         const int n0 = (t % a.tiles_n) * BN;
+        int iw0 = 0, ih0 = 0, img = 0;
+        if (!GATHER && a.a_im2col) {
+          img = m0 / a.OHW;
+          const int rem = m0 - img * a.OHW;
+          const int oh = rem / a.OW;
+          ih0 = oh * a.stride - a.pad;
+          iw0 = (rem - oh * a.OW) * a.stride - a.pad;
+        }
         for (int kb = 0; kb < a.kblocks + a.res_kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (kb >= a.kblocks) {
@@ -237,6 +246,14 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
           } else {
             if (GATHER) {
               mbar_arrive_expect_tx(&full[stage], Cfg::B_BYTES);
+            } else if (a.a_im2col) {
+              mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
+              const int tap = kb / cpb;
+              const int c0 = (kb - tap * cpb) << 6;
+              const int r = tap / a.S;
+              const int s = tap - r * a.S;
+              tma_load_im2col_4d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], c0, iw0, ih0,
+                                 img, (uint16_t)s, (uint16_t)r);
             } else {
               mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
               tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * TC_BK, m0);

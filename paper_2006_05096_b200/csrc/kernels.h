@@ -31,6 +31,7 @@ struct TcArgs {
   int tma_epi;          // epilogue through smem + TMA store (N % 8 == 0, BN >= 64)
   int stages;           // smem pipeline depth (0 = the most that fits)
   int epi_debug;        // 0 normal; 1 drain TMEM only (no math/stores) — profiling aid
+  int a_im2col;         // A via TMA im2col mode (C % 64 == 0 convs): tmA is an im2col map
   int res_kblocks;      // >0: residual folded into the MMA as [A | res] x [W | I]^T;
                         // BN/64 extra K blocks per tile, A from tmR, B from the identity
 };

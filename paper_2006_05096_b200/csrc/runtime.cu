@@ -123,6 +123,48 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t co
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const int*, const int*,
+                                   cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                   CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeIm2colFn encode_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(p);
+  }
+  return fn;
+}
+
+// NHWC bf16 activation [N, H, W, C] for implicit-GEMM conv A tiles: 128 output
+// pixels x 64 channels per load, filter offsets supplied per load
+bool make_tmap_im2col(CUtensorMap* m, const void* base, int N, int H, int W, int C, int R, int S,
+                      int stride, int pad) {
+  EncodeIm2colFn fn = encode_im2col_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+  int lower[2] = {-pad, -pad};
+  int upper[2] = {pad - (S - 1), pad - (R - 1)};
+  cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+  if (fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, lower,
+         upper, 64, 128, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  // driver <= 13.1 workaround for tensors under 128 KB (mirrors CUTLASS)
+  int drv = 0;
+  cudaDriverGetVersion(&drv);
+  if (drv <= 13010 && (uint64_t)N * H * W * C * 2 < 131072)
+    reinterpret_cast<uint64_t*>(m)[1] &= ~(1ull << 21);
+  return true;
+}
+
 // ------------------------------------------------------------------ executor state
 struct Layer {
   int kind;
@@ -136,6 +178,7 @@ struct Layer {
   void* w3 = nullptr;       // embed: type row (T)
   // GEMM execution choices
   bool tc = false, gather = false;
+  bool im2col = false;      // A via TMA im2col (C % 64 == 0 convs)
   int gmode = 0;            // see TcArgs::gmode
   int K = 0, kpad = 0, ldw = 0;
 };
@@ -178,6 +221,7 @@ struct b2_plan {
   int launches = 0;
   int epi_mode = 0;          // B2_EPI_MODE: 0 TMA-store epilogue, 1 drain-only, 2 direct stores
   int fold_max_k = 256;      // B2_FOLD_MAX_K: fold residuals into the MMA when K <= this
+  bool use_im2col = true;    // B2_IM2COL=0 -> cp.async gather for C % 64 == 0 convs
   void* identity = nullptr;  // bf16 I[256][256]
   int stages_override = 0;   // B2_STAGES
 };
@@ -251,6 +295,10 @@ int upload_weights(b2_plan* pl, const uint8_t* data, const std::vector<WeightRec
           const int R = conv ? L.p[8] : 1, S = conv ? L.p[9] : 1;
           const bool pow2 = (C & (C - 1)) == 0;
           L.gmode = !L.gather ? 0 : (C % 64 == 0) ? 1 : (S * C <= 64 && pow2) ? 2 : 3;
+          if (L.gmode == 1 && pl->use_im2col) {
+            L.im2col = true;     // TMA im2col producer instead of the cp.async gather
+            L.gather = false;
+          }
           L.kpad = L.gmode == 2 ? R * 64 : (K + 63) / 64 * 64;
           L.ldw = L.kpad;
           std::vector<float> h((size_t)N * L.kpad, 0.f);
@@ -409,7 +457,8 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
           const int bn = S.bn[li];
           a.tiles_m = (int)((M + 127) / 128);
           a.tiles_n = (N + bn - 1) / bn;
-          if (L.gather) {
+          if (L.gather || L.im2col) {
+            a.a_im2col = L.im2col;
             a.x = reinterpret_cast<const bf16*>(S.act[p[0]]);
             a.H = p[4];
             a.W = p[5];
@@ -584,7 +633,11 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
         return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeTiled(res/identity) failed", li);
       S.fold[li] = 1;
     }
-    if (!L.gather) {
+    if (L.im2col) {
+      if (!make_tmap_im2col(&S.tmA[li], S.act[p[0]], batch, p[4], p[5], p[6], p[8], p[9], p[10],
+                            p[11]))
+        return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeIm2col failed", li);
+    } else if (!L.gather) {
       const int K = L.K;
       const long ld = conv ? p[6] : p[9];
       if ((ld * 2) % 16 != 0) return fail(B2_ERR_UNSUPPORTED, "layer %zu: A pitch not 16B", li);
@@ -680,6 +733,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* em = getenv("B2_EPI_MODE")) pl->epi_mode = atoi(em);
   if (const char* sg = getenv("B2_STAGES")) pl->stages_override = atoi(sg);
   if (const char* fk = getenv("B2_FOLD_MAX_K")) pl->fold_max_k = atoi(fk);
+  if (const char* ic = getenv("B2_IM2COL")) pl->use_im2col = ic[0] != '0';
   cudaGetDevice(&pl->device);
   cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, pl->device);
   int major = 0;
