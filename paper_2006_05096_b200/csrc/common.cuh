@@ -235,6 +235,18 @@ B2_DEV uint64_t smem_desc_sw128(uint32_t smem_addr) {
   return d;
 }
 
+// K-major operand in the non-swizzled ("interleave") canonical layout: core
+// matrices of 8 rows x 16 B stored contiguously (128 B); `lbo` = byte stride
+// between core matrices along K, `sbo` = byte stride between 8-row groups.
+B2_DEV uint64_t smem_desc_kmajor_noswizzle(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;   // layout type 0 = SWIZZLE_NONE
+}
+
 // instruction descriptor: fp32 accumulate, A/B format fmt (1 = bf16, 2 = tf32),
 // both K-major, shape M x N
 __host__ __device__ constexpr uint32_t make_idesc(int M, int N, uint32_t fmt) {

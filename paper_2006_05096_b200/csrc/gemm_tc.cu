@@ -246,6 +246,20 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
           } else {
             if (GATHER) {
               mbar_arrive_expect_tx(&full[stage], Cfg::B_BYTES);
+            } else if (a.a_im2col == 2) {
+              // 8 taps x (128 pixels x 8 channels); taps past R*S load tap 0
+              // (finite data) against zero weights
+              mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
+              const int ntaps = a.R * a.S;
+#pragma unroll 1
+              for (int j = 0; j < 8; ++j) {
+                int tap = kb * 8 + j;
+                if (tap >= ntaps) tap = 0;
+                const int r = tap / a.S;
+                const int s = tap - r * a.S;
+                tma_load_im2col_4d(sA + stage * Cfg::A_BYTES + j * 2048, &tmA, &full[stage], 0,
+                                   iw0, ih0, img, (uint16_t)s, (uint16_t)r);
+              }
             } else if (a.a_im2col) {
               mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
               const int tap = kb / cpb;
@@ -283,11 +297,15 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
         for (int kb = 0; kb < a.kblocks + a.res_kblocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint64_t ad = smem_desc_sw128(smem_u32(sA + stage * Cfg::A_BYTES));
+          const bool tap8 = a.a_im2col == 2 && kb < a.kblocks;
+          const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint64_t ad = tap8 ? smem_desc_kmajor_noswizzle(a_addr, 2048, 128)
+                                   : smem_desc_sw128(a_addr);
+          const uint32_t astep = tap8 ? 256u : 2u;   // K += 16: 2 taps (4 KB) or 32 B
           const uint64_t bd = smem_desc_sw128(smem_u32(sB + stage * Cfg::B_BYTES));
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k)
-            umma_bf16(dt, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_bf16(dt, ad + astep * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
           umma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;

@@ -24,6 +24,7 @@ struct TcArgs {
   // gather (implicit im2col) parameters, NHWC input
   const bf16* x;
   int H, W, C, OW, OHW, S, stride, pad;
+  int R;
   int gmode;            // 1: C % 64 == 0 (one filter tap per K block)
                         // 2: S*C <= 64, C = 2^c_log2 (one filter row per K block)
                         // 3: generic (per-chunk tap decomposition)
@@ -31,7 +32,9 @@ struct TcArgs {
   int tma_epi;          // epilogue through smem + TMA store (N % 8 == 0, BN >= 64)
   int stages;           // smem pipeline depth (0 = the most that fits)
   int epi_debug;        // 0 normal; 1 drain TMEM only (no math/stores) — profiling aid
-  int a_im2col;         // A via TMA im2col mode (C % 64 == 0 convs): tmA is an im2col map
+  int a_im2col;         // A via TMA im2col: 1 = 64-channel boxes (C % 64 == 0, 128B swizzle);
+                        // 2 = one 8-channel filter tap per 2 KB box (C == 8 stems), 8 taps
+                        //     per K block in the non-swizzled K-major layout
   int res_kblocks;      // >0: residual folded into the MMA as [A | res] x [W | I]^T;
                         // BN/64 extra K blocks per tile, A from tmR, B from the identity
 };

@@ -145,7 +145,7 @@ EncodeIm2colFn encode_im2col_fn() {
 // NHWC bf16 activation [N, H, W, C] for implicit-GEMM conv A tiles: 128 output
 // pixels x 64 channels per load, filter offsets supplied per load
 bool make_tmap_im2col(CUtensorMap* m, const void* base, int N, int H, int W, int C, int R, int S,
-                      int stride, int pad) {
+                      int stride, int pad, int cpp) {
   EncodeIm2colFn fn = encode_im2col_fn();
   if (!fn) return false;
   cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
@@ -154,7 +154,8 @@ bool make_tmap_im2col(CUtensorMap* m, const void* base, int N, int H, int W, int
   int upper[2] = {pad - (S - 1), pad - (R - 1)};
   cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
   if (fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, lower,
-         upper, 64, 128, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+         upper, (cuuint32_t)cpp, 128, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         cpp == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
   // driver <= 13.1 workaround for tensors under 128 KB (mirrors CUTLASS)
@@ -178,7 +179,8 @@ struct Layer {
   void* w3 = nullptr;       // embed: type row (T)
   // GEMM execution choices
   bool tc = false, gather = false;
-  bool im2col = false;      // A via TMA im2col (C % 64 == 0 convs)
+  bool im2col = false;      // A via TMA im2col (C % 64 == 0 convs, or C == 8 stems)
+  int im2col_mode = 0;      // TcArgs::a_im2col
   int gmode = 0;            // see TcArgs::gmode
   int K = 0, kpad = 0, ldw = 0;
 };
@@ -222,6 +224,8 @@ struct b2_plan {
   int epi_mode = 0;          // B2_EPI_MODE: 0 TMA-store epilogue, 1 drain-only, 2 direct stores
   int fold_max_k = 256;      // B2_FOLD_MAX_K: fold residuals into the MMA when K <= this
   bool use_im2col = true;    // B2_IM2COL=0 -> cp.async gather for C % 64 == 0 convs
+  bool im2col8 = false;      // B2_IM2COL8=1 -> 8-channel-tap im2col TMA for C == 8 stems
+                             // (correct, but issue-bound on 2 KB boxes: slower than gather)
   void* identity = nullptr;  // bf16 I[256][256]
   int stages_override = 0;   // B2_STAGES
 };
@@ -295,9 +299,13 @@ int upload_weights(b2_plan* pl, const uint8_t* data, const std::vector<WeightRec
           const int R = conv ? L.p[8] : 1, S = conv ? L.p[9] : 1;
           const bool pow2 = (C & (C - 1)) == 0;
           L.gmode = !L.gather ? 0 : (C % 64 == 0) ? 1 : (S * C <= 64 && pow2) ? 2 : 3;
-          if (L.gmode == 1 && pl->use_im2col) {
+          if (L.gather && (L.gmode == 1 || (C == 8 && pl->im2col8)) && pl->use_im2col) {
             L.im2col = true;     // TMA im2col producer instead of the cp.async gather
             L.gather = false;
+            L.im2col_mode = C == 8 ? 2 : 1;
+            if (C == 8) L.gmode = 3;   // generic (r, s, c) K order, K padded to 64
+            L.kpad = (K + 63) / 64 * 64;
+            L.ldw = L.kpad;
           }
           L.kpad = L.gmode == 2 ? R * 64 : (K + 63) / 64 * 64;
           L.ldw = L.kpad;
@@ -402,7 +410,9 @@ int validate_ops(b2_plan* pl) {
       case OP_ATTENTION: ok = tok(p[0]) && tok(p[1]) && p[3] == 64; break;
       case OP_OUTPUT: {
         ok = p[0] >= 1 && p[0] <= 15;
-        for (int j = 0; ok && j < p[0]; ++j) ok = tok(p[1 + 2 * j]);
+        for (int j = 0; ok && j < p[0]; ++j)
+          ok = tok(p[1 + 2 * j]) && p[2 + 2 * j] >= 0 &&
+               p[2 + 2 * j] + (long)pl->tensors[p[1 + 2 * j]].elems <= pl->out_elems;
         break;
       }
       default: return fail(B2_ERR_UNSUPPORTED, "op %zu: unknown kind %d", i, L.kind);
@@ -458,7 +468,8 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
           a.tiles_m = (int)((M + 127) / 128);
           a.tiles_n = (N + bn - 1) / bn;
           if (L.gather || L.im2col) {
-            a.a_im2col = L.im2col;
+            a.a_im2col = L.im2col ? L.im2col_mode : 0;
+            a.R = p[8];
             a.x = reinterpret_cast<const bf16*>(S.act[p[0]]);
             a.H = p[4];
             a.W = p[5];
@@ -635,7 +646,7 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     }
     if (L.im2col) {
       if (!make_tmap_im2col(&S.tmA[li], S.act[p[0]], batch, p[4], p[5], p[6], p[8], p[9], p[10],
-                            p[11]))
+                            p[11], L.im2col_mode == 2 ? 8 : 64))
         return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeIm2col failed", li);
     } else if (!L.gather) {
       const int K = L.K;
@@ -734,6 +745,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* sg = getenv("B2_STAGES")) pl->stages_override = atoi(sg);
   if (const char* fk = getenv("B2_FOLD_MAX_K")) pl->fold_max_k = atoi(fk);
   if (const char* ic = getenv("B2_IM2COL")) pl->use_im2col = ic[0] != '0';
+  if (const char* i8 = getenv("B2_IM2COL8")) pl->im2col8 = i8[0] == '1';
   cudaGetDevice(&pl->device);
   cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, pl->device);
   int major = 0;

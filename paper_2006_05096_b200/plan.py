@@ -261,6 +261,12 @@ def decode(blob: bytes) -> Plan:
         kind, *p = _OP.unpack_from(blob, pos)
         pos += _OP.size
         ops.append(Op(kind, list(p)))
+    for o in ops:
+        if o.kind == OP_OUTPUT:
+            for j in range(o.p[0]):
+                t, off = o.p[1 + 2 * j], o.p[2 + 2 * j]
+                if not (0 <= t < nt) or off < 0 or off + tensors[t].elems > out_elems:
+                    raise PlanFormatError("OUTPUT op writes outside the output row")
     meta = json.loads(blob[pos:pos + meta_len].decode()) if meta_len else {}
     pos = _align(pos + meta_len)
     weights = []

@@ -13,7 +13,7 @@ b.op_p(P.OP_INPUT, [x, C, H, W, C])
 rng = np.random.default_rng(0)
 y = b.tensor(OH, OW, Cout)
 b.op_p(P.OP_CONV, [x, y, b.weight(rng.standard_normal((Cout, Rk, Rk, C)) * 0.05), b.weight(np.zeros(Cout)), H, W, C, Cout, Rk, Rk, st, pad, OH, OW, 1, -1])
-b.out_elems = 1
+b.out_elems = b.tensors[y].elems
 b.op_p(P.OP_OUTPUT, [1, y, 0])
 plan = R.Plan(b.build(P.DT_BF16), P.DT_BF16)
 prof = plan.profile_ops(B, iters=5)

@@ -16,7 +16,7 @@ if res:
     b.op_p(P.OP_LINEAR, [x, r, b.weight(rng.standard_normal((N, K)) * 0.1), b.weight(np.zeros(N)), K, N, 1, 0, -1, K])
 y = b.tensor(N)
 b.op_p(P.OP_LINEAR, [x, y, b.weight(rng.standard_normal((N, K)) * 0.1), b.weight(np.zeros(N)), K, N, 1, 1, r, K])
-b.out_elems = 1
+b.out_elems = b.tensors[y].elems
 b.op_p(P.OP_OUTPUT, [1, b.tensor(1) if False else y, 0])
 blob = b.build(P.DT_BF16)
 plan = R.Plan(blob, P.DT_BF16)
