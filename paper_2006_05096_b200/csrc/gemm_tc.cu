@@ -155,7 +155,10 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint
       if (a.epi_debug != 3) fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0 && a.epi_debug != 5) {
-        tma_store_2d(&tmO, obuf + (oi & 1) * 2048, n0 + c, row0);
+        if (a.out3d)
+          tma_store_3d(&tmO, obuf + (oi & 1) * 2048, n0 + c, lg * 32, m0 / TC_BM);
+        else
+          tma_store_2d(&tmO, obuf + (oi & 1) * 2048, n0 + c, row0);
         bulk_commit();
       }
       ++oi;
@@ -246,6 +249,13 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
           } else {
             if (GATHER) {
               mbar_arrive_expect_tx(&full[stage], Cfg::B_BYTES);
+            } else if (a.a_im2col == 3) {
+              // s2d stem: tile = output row (img, oh); K block kb = filter row-pair
+              mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
+              const int rt = m0 / TC_BM;
+              const int im = rt / a.OH;
+              tma_load_4d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], 0, 0,
+                          rt - im * a.OH + kb, im);
             } else if (a.a_im2col == 2) {
               // 8 taps x (128 pixels x 8 channels); taps past R*S load tap 0
               // (finite data) against zero weights

@@ -144,6 +144,42 @@ cudaError_t input_pack(const float* in, T* out, int B, int C, int H, int W, int 
   return cudaGetLastError();
 }
 
+// 2x2 space-to-depth pack for stride-2 stems: out[n][Y][X][q], q = (dy*2+dx)*4 + c,
+// holds in[n][c][2Y+dy-shift][2X+dx-shift] (zero outside the image / for c >= C).
+__global__ void input_pack_s2d_kernel(const float* __restrict__ in, bf16* __restrict__ out, int B,
+                                      int C, int H, int W, int shift, int H2, int W2) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;   // over B*H2*W2
+  if (i >= (long)B * H2 * W2) return;
+  const int X = (int)(i % W2);
+  const long t = i / W2;
+  const int Y = (int)(t % H2);
+  const long n = t / H2;
+  uint32_t w[8];
+#pragma unroll
+  for (int qq = 0; qq < 8; ++qq) {
+    float v2[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = qq * 2 + h;
+      const int c = q & 3, dx = (q >> 2) & 1, dy = q >> 3;
+      const int y = 2 * Y + dy - shift, x = 2 * X + dx - shift;
+      v2[h] = (c < C && (unsigned)y < (unsigned)H && (unsigned)x < (unsigned)W)
+                  ? __ldg(in + ((n * C + c) * H + y) * (long)W + x)
+                  : 0.f;
+    }
+    w[qq] = pack_bf16x2(v2[0], v2[1]);
+  }
+  uint4* o = reinterpret_cast<uint4*>(out + i * 16);
+  o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  o[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+cudaError_t input_pack_s2d(const float* in, bf16* out, int B, int C, int H, int W, int shift,
+                           int H2, int W2, cudaStream_t st) {
+  input_pack_s2d_kernel<<<nblk((long)B * H2 * W2, 256), 256, 0, st>>>(in, out, B, C, H, W, shift,
+                                                                      H2, W2);
+  return cudaGetLastError();
+}
+
 __global__ void tokens_kernel(const int64_t* in, int32_t* out, long n, int vocab) {
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;

@@ -32,7 +32,11 @@ struct TcArgs {
   int tma_epi;          // epilogue through smem + TMA store (N % 8 == 0, BN >= 64)
   int stages;           // smem pipeline depth (0 = the most that fits)
   int epi_debug;        // 0 normal; 1 drain TMEM only (no math/stores) — profiling aid
-  int a_im2col;         // A via TMA im2col: 1 = 64-channel boxes (C % 64 == 0, 128B swizzle);
+  int OH;               // s2d stems: output rows per image (M tile = one output row)
+  int out3d;            // output TMA map is [rows, OW, C]: box rows clip at OW
+  int a_im2col;         // A via TMA: 3 = space-to-depth stem (one output row per M tile,
+                        //     tiled 4D view with overlapping pixel stride, K block = filter row);
+                        // 1 = 64-channel im2col boxes (C % 64 == 0, 128B swizzle);
                         // 2 = one 8-channel filter tap per 2 KB box (C == 8 stems), 8 taps
                         //     per K block in the non-swizzled K-major layout
   int res_kblocks;      // >0: residual folded into the MMA as [A | res] x [W | I]^T;
@@ -65,6 +69,8 @@ template <typename T> cudaError_t gemm_simt(const GemmSimtArgs& a, cudaStream_t 
 template <typename T>
 cudaError_t input_pack(const float* in, T* out, int B, int C, int H, int W, int Cp,
                        cudaStream_t st);
+cudaError_t input_pack_s2d(const float* in, bf16* out, int B, int C, int H, int W, int shift,
+                           int H2, int W2, cudaStream_t st);
 cudaError_t tokens_pack(const int64_t* in, int32_t* out, long n, int vocab, cudaStream_t st);
 template <typename T>
 cudaError_t dwconv(const T* x, const T* w_rsc, const float* bias, T* y, int B, int H, int W,

@@ -180,6 +180,10 @@ struct Layer {
   // GEMM execution choices
   bool tc = false, gather = false;
   bool im2col = false;      // A via TMA im2col (C % 64 == 0 convs, or C == 8 stems)
+  // space-to-depth stem (conv) / producer (input): stride-2 conv on <= 4 real
+  // channels re-expressed as a stride-1 conv on a 2x2 space-to-depth tensor
+  bool s2d = false;
+  int s2d_shift = 0, s2d_H2 = 0, s2d_W2 = 0, s2d_Rp = 0, s2d_creal = 0;
   int im2col_mode = 0;      // TcArgs::a_im2col
   int gmode = 0;            // see TcArgs::gmode
   int K = 0, kpad = 0, ldw = 0;
@@ -224,6 +228,7 @@ struct b2_plan {
   int epi_mode = 0;          // B2_EPI_MODE: 0 TMA-store epilogue, 1 drain-only, 2 direct stores
   int fold_max_k = 256;      // B2_FOLD_MAX_K: fold residuals into the MMA when K <= this
   bool use_im2col = true;    // B2_IM2COL=0 -> cp.async gather for C % 64 == 0 convs
+  bool use_s2d = true;       // B2_S2D=0 -> stems on the cp.async gather path
   bool im2col8 = false;      // B2_IM2COL8=1 -> 8-channel-tap im2col TMA for C == 8 stems
                              // (correct, but issue-bound on 2 KB boxes: slower than gather)
   void* identity = nullptr;  // bf16 I[256][256]
@@ -260,6 +265,48 @@ template <typename T> int upload_as(b2_plan* pl, const std::vector<float>& h, vo
   pl->weight_bytes += h.size() * sizeof(T);
   *out = d;
   return B2_OK;
+}
+
+// Find stride-2 stems fed directly by the INPUT op (<= 4 real channels, odd
+// square filter, "same" padding, even H/W, one output row fits an M tile) and
+// switch them and their INPUT op to the space-to-depth layout.
+void plan_s2d(b2_plan* pl) {
+  if (pl->dtype != B2_DT_BF16 || pl->force_simt || !pl->use_s2d) return;
+  for (size_t ci = 0; ci < pl->layers.size(); ++ci) {
+    Layer& Lc = pl->layers[ci];
+    if (Lc.kind != OP_CONV) continue;
+    const int* p = Lc.p;
+    const int R = p[8], S = p[9], stride = p[10], pad = p[11];
+    if (stride != 2 || R != S || (R & 1) == 0 || pad != (R - 1) / 2 || (p[4] & 1) ||
+        (p[5] & 1) || p[13] > 128 || p[15] >= 0)
+      continue;
+    int in_op = -1, consumers = 0;
+    for (size_t j = 0; j < pl->layers.size(); ++j) {
+      const Layer& Lj = pl->layers[j];
+      if (Lj.kind == OP_INPUT && Lj.p[0] == p[0]) in_op = (int)j;
+      if (Lj.kind == OP_OUTPUT) {
+        for (int q = 0; q < Lj.p[0]; ++q) consumers += Lj.p[1 + 2 * q] == p[0];
+      } else if (Lj.kind != OP_INPUT && Lj.p[0] == p[0]) {
+        ++consumers;
+      } else if ((Lj.kind == OP_CONV && Lj.p[15] == p[0]) ||
+                 ((Lj.kind == OP_LINEAR) && Lj.p[8] == p[0]) ||
+                 (Lj.kind == OP_LAYERNORM && Lj.p[7] == p[0])) {
+        ++consumers;
+      }
+    }
+    if (in_op < 0 || consumers != 1) continue;
+    Layer& Li = pl->layers[in_op];
+    if (Li.p[1] > 4 || Li.p[4] != p[6]) continue;
+    const int Rp = R / 2 + 1;
+    for (Layer* L : {&Lc, &Li}) {
+      L->s2d = true;
+      L->s2d_shift = pad + 1;
+      L->s2d_Rp = Rp;
+      L->s2d_H2 = p[12] + Rp - 1;
+      L->s2d_W2 = p[13] + 3;
+      L->s2d_creal = Li.p[1];
+    }
+  }
 }
 
 int upload_weights(b2_plan* pl, const uint8_t* data, const std::vector<WeightRec>& wr,
@@ -308,9 +355,26 @@ int upload_weights(b2_plan* pl, const uint8_t* data, const std::vector<WeightRec
             L.ldw = L.kpad;
           }
           L.kpad = L.gmode == 2 ? R * 64 : (K + 63) / 64 * 64;
+          if (L.s2d) {
+            L.gather = false;
+            L.im2col = false;
+            L.kpad = L.s2d_Rp * 64;
+          }
           L.ldw = L.kpad;
           std::vector<float> h((size_t)N * L.kpad, 0.f);
-          if (L.gmode == 2) {   // [N][R][64]: each filter row's (s, c) run padded to 64
+          if (L.s2d) {
+            // W''[n][r'][s'][q], q = (dy*2+dx)*4 + c  <-  W[n][2r'+dy-1][2s'+dx-1][c]
+            for (int n = 0; n < N; ++n)
+              for (int rp = 0; rp < L.s2d_Rp; ++rp)
+                for (int sp = 0; sp < 4; ++sp)
+                  for (int q = 0; q < 16; ++q) {
+                    const int c = q & 3, dx = (q >> 2) & 1, dy = q >> 3;
+                    const int r = 2 * rp + dy - 1, ss = 2 * sp + dx - 1;
+                    if (c >= L.s2d_creal || r < 0 || r >= R || ss < 0 || ss >= S) continue;
+                    h[(size_t)n * L.kpad + rp * 64 + sp * 16 + q] =
+                        w[(size_t)n * K + ((size_t)r * S + ss) * C + c];
+                  }
+          } else if (L.gmode == 2) {   // [N][R][64]: each filter row's (s, c) run padded to 64
             for (int n = 0; n < N; ++n)
               for (int r = 0; r < R; ++r)
                 memcpy(&h[(size_t)n * L.kpad + r * 64], w + (size_t)n * K + (size_t)r * S * C,
@@ -435,7 +499,12 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
     if (op_events) CK(cudaEventRecord(op_events[li], st));
     switch (L.kind) {
       case OP_INPUT:
-        CK(input_pack<T>(static_cast<const float*>(d_in), A(p[0]), B, p[1], p[2], p[3], p[4], st));
+        if (L.s2d)
+          CK(input_pack_s2d(static_cast<const float*>(d_in), reinterpret_cast<bf16*>(S.act[p[0]]),
+                            B, p[1], p[2], p[3], L.s2d_shift, L.s2d_H2, L.s2d_W2, st));
+        else
+          CK(input_pack<T>(static_cast<const float*>(d_in), A(p[0]), B, p[1], p[2], p[3], p[4],
+                           st));
         ++launches;
         break;
       case OP_TOKENS:
@@ -466,6 +535,12 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
           a.act = act;
           const int bn = S.bn[li];
           a.tiles_m = (int)((M + 127) / 128);
+          if (L.s2d) {
+            a.tiles_m = B * p[12];     // one output row per M tile
+            a.OH = p[12];
+            a.out3d = 1;
+            a.a_im2col = 3;
+          }
           a.tiles_n = (N + bn - 1) / bn;
           if (L.gather || L.im2col) {
             a.a_im2col = L.im2col ? L.im2col_mode : 0;
@@ -597,7 +672,10 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
   S.batch = batch;
   S.act.resize(pl->tensors.size(), nullptr);
   for (size_t t = 0; t < pl->tensors.size(); ++t) {
-    const size_t bytes = (size_t)batch * pl->tensors[t].elems * elem_size(pl, (int)t);
+    size_t bytes = (size_t)batch * pl->tensors[t].elems * elem_size(pl, (int)t);
+    for (const Layer& L : pl->layers)   // space-to-depth input: [B, H2, W2, 16] bf16
+      if (L.kind == OP_INPUT && L.s2d && L.p[0] == (int)t)
+        bytes = (size_t)batch * L.s2d_H2 * L.s2d_W2 * 16 * 2;
     CK(cudaMalloc(&S.act[t], bytes + 256));
     CK(cudaMemset(S.act[t], 0, bytes + 256));
   }
@@ -629,6 +707,29 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     if (!make_tmap_bf16(&S.tmB[li], L.w, (uint64_t)N, (uint64_t)L.kpad, (uint64_t)L.kpad * 2,
                         (uint32_t)bn))
       return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeTiled(B) failed", li);
+    if (L.s2d) {
+      // A: overlapping 4D view of the space-to-depth input — element (k, ow, Y, n)
+      // at ((n*H2 + Y)*W2 + ow)*16 + k: one 128 B row = 4 pixel columns x 16 ch
+      EncodeTiledFn fn = encode_fn();
+      cuuint64_t dims[4] = {64, (cuuint64_t)p[13], (cuuint64_t)L.s2d_H2, (cuuint64_t)batch};
+      cuuint64_t str[3] = {32, (cuuint64_t)L.s2d_W2 * 32, (cuuint64_t)L.s2d_H2 * L.s2d_W2 * 32};
+      cuuint32_t box[4] = {64, 128, 1, 1};
+      cuuint32_t es[4] = {1, 1, 1, 1};
+      // out: [B*OH, OW, N] so the 32-row store boxes clip at the row end
+      cuuint64_t odims[3] = {(cuuint64_t)N, (cuuint64_t)p[13], (cuuint64_t)batch * p[12]};
+      cuuint64_t ostr[2] = {(cuuint64_t)N * 2, (cuuint64_t)N * p[13] * 2};
+      cuuint32_t obox[3] = {32, 32, 1};
+      cuuint32_t oes[3] = {1, 1, 1};
+      if (!fn || N % 8 != 0 || bn < 32 ||
+          fn(&S.tmA[li], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, S.act[p[0]], dims, str, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+          fn(&S.tmO[li], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, S.act[p[1]], odims, ostr, obox, oes,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return fail(B2_ERR_CUDA, "layer %zu: space-to-depth tensor maps rejected", li);
+      continue;
+    }
     if (bn >= 32 && N % 8 == 0) {
       if (!make_tmap_bf16(&S.tmO[li], S.act[p[1]], (uint64_t)M, (uint64_t)N, (uint64_t)N * 2, 32,
                           32, CU_TENSOR_MAP_SWIZZLE_64B))
@@ -746,6 +847,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* fk = getenv("B2_FOLD_MAX_K")) pl->fold_max_k = atoi(fk);
   if (const char* ic = getenv("B2_IM2COL")) pl->use_im2col = ic[0] != '0';
   if (const char* i8 = getenv("B2_IM2COL8")) pl->im2col8 = i8[0] == '1';
+  if (const char* sd = getenv("B2_S2D")) pl->use_s2d = sd[0] != '0';
   cudaGetDevice(&pl->device);
   cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, pl->device);
   int major = 0;
@@ -776,6 +878,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
     return fail(B2_ERR_FORMAT, "truncated weight data");
   }
   int rc = validate_ops(pl);
+  if (!rc) plan_s2d(pl);
   if (!rc) rc = upload_weights(pl, d + pos, wr, len - 4 - pos);
   if (!rc && pl->dtype == B2_DT_BF16) {
     std::vector<float> eye(256 * 256, 0.f);
@@ -956,6 +1059,24 @@ int b2_read_tensor(b2_plan* pl, int batch, int tensor, void* host_out, size_t by
   int rc = check_device(pl);
   if (rc) return rc;
   CK(cudaStreamSynchronize(pl->stream));
+  for (const Layer& L : pl->layers) {
+    if (L.kind != OP_INPUT || !L.s2d || L.p[0] != tensor) continue;
+    // logical NHWC [B, H, W, Cpad] view of the space-to-depth storage
+    const int H = L.p[2], W = L.p[3], Cp = L.p[4], H2 = L.s2d_H2, W2 = L.s2d_W2;
+    std::vector<uint16_t> raw((size_t)batch * H2 * W2 * 16);
+    CK(cudaMemcpy(raw.data(), it->second.act[tensor], raw.size() * 2, cudaMemcpyDeviceToHost));
+    uint16_t* o = static_cast<uint16_t*>(host_out);
+    for (int n = 0; n < batch; ++n)
+      for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x)
+          for (int c = 0; c < Cp; ++c) {
+            const int yy = y + L.s2d_shift, xx = x + L.s2d_shift;
+            const int q = ((yy & 1) * 2 + (xx & 1)) * 4 + c;
+            o[(((size_t)n * H + y) * W + x) * Cp + c] =
+                c < 4 ? raw[(((size_t)n * H2 + (yy >> 1)) * W2 + (xx >> 1)) * 16 + q] : 0;
+          }
+    return B2_OK;
+  }
   CK(cudaMemcpy(host_out, it->second.act[tensor], need, cudaMemcpyDeviceToHost));
   return B2_OK;
 }

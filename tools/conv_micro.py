@@ -8,11 +8,11 @@ B, H, W, C, Cout, Rk, st = [int(v) for v in sys.argv[1:8]]
 pad = Rk // 2
 OH = (H + 2 * pad - Rk) // st + 1; OW = (W + 2 * pad - Rk) // st + 1
 b = P.PlanBuilder("cmicro")
-x = b.tensor(H, W, C); b.in_elems = C * H * W
-b.op_p(P.OP_INPUT, [x, C, H, W, C])
+Cp = max(8, C); x = b.tensor(H, W, Cp); b.in_elems = C * H * W
+b.op_p(P.OP_INPUT, [x, C, H, W, Cp])
 rng = np.random.default_rng(0)
 y = b.tensor(OH, OW, Cout)
-b.op_p(P.OP_CONV, [x, y, b.weight(rng.standard_normal((Cout, Rk, Rk, C)) * 0.05), b.weight(np.zeros(Cout)), H, W, C, Cout, Rk, Rk, st, pad, OH, OW, 1, -1])
+b.op_p(P.OP_CONV, [x, y, b.weight(rng.standard_normal((Cout, Rk, Rk, Cp)) * 0.05), b.weight(np.zeros(Cout)), H, W, Cp, Cout, Rk, Rk, st, pad, OH, OW, 1, -1])
 b.out_elems = b.tensors[y].elems
 b.op_p(P.OP_OUTPUT, [1, y, 0])
 plan = R.Plan(b.build(P.DT_BF16), P.DT_BF16)
