@@ -5,7 +5,7 @@ activation tensors, plus fp32 weights.  It is the on-disk format between the
 converter plugins (the reference's ConverterPlugin boundary,
 pkg/src/modelci/converter/plugins.py:32-68) and the executor (the reference's
 MockServer, pkg/src/modelci/mockserve/server.py:94-127).  The byte layout is
-mirrored in C++ by paper_2006_05096_b200/csrc/plan.cpp and in numpy by
+mirrored in C++ by paper_2006_05096_b200/csrc/runtime.cu (b2_plan_create) and in numpy by
 oracle/plan_ref.py.
 
 Layout (little endian):
