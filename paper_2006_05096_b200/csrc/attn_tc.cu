@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(128, 2)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 81920);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = warp_index_uniform(), lane = threadIdx.x & 31;
   const int b = blockIdx.x / H, h = blockIdx.x % H;
   const int row0 = b * AT_S;
 
@@ -58,21 +58,24 @@ __global__ void __launch_bounds__(128, 2)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = *tslot;
+  const uint32_t tbase = uniform_u32(*tslot);
 
-  if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(&bars[0], 3 * 16384);
-    tma_load_2d(sQ, &tmQKV, &bars[0], h * AT_D, row0);
-    tma_load_2d(sK, &tmQKV, &bars[0], (H + h) * AT_D, row0);
-    tma_load_2d(sV, &tmQKV, &bars[0], (2 * H + h) * AT_D, row0);
+  if (warp == 0) {   // converged warp, elected lane issues (common.cuh)
+    if (elect_one()) {
+      mbar_arrive_expect_tx(&bars[0], 3 * 16384);
+      tma_load_2d(sQ, &tmQKV, &bars[0], h * AT_D, row0);
+      tma_load_2d(sK, &tmQKV, &bars[0], (H + h) * AT_D, row0);
+      tma_load_2d(sV, &tmQKV, &bars[0], (2 * H + h) * AT_D, row0);
+    }
+    __syncwarp();
     mbar_wait(&bars[0], 0);
     tc_fence_after();
     const uint64_t dq = smem_desc_sw128(smem_u32(sQ));
     const uint64_t dk = smem_desc_sw128(smem_u32(sK));
 #pragma unroll
     for (int k = 0; k < AT_D / 16; ++k)
-      umma_bf16(tbase, dq + 2 * k, dk + 2 * k, make_idesc(128, 128, 1u), k ? 1u : 0u);
-    umma_commit(&bars[1]);
+      if (elect_one()) umma_bf16(tbase, dq + 2 * k, dk + 2 * k, make_idesc(128, 128, 1u), k ? 1u : 0u);
+    if (elect_one()) umma_commit(&bars[1]);
   }
   mbar_wait(&bars[1], 0);
   tc_fence_after();
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(128, 2)
   tc_fence_before();
   __syncthreads();
 
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
     tc_fence_after();
     const uint32_t pbase = smem_u32(sP);
     const uint32_t vbase = smem_u32(sV);
@@ -124,9 +127,9 @@ __global__ void __launch_bounds__(128, 2)
     for (int k = 0; k < AT_S / 16; ++k) {
       const uint64_t da = smem_desc_sw128(pbase + (k >> 2) * 16384 + (k & 3) * 32);
       const uint64_t dv = smem_desc_mn_sw128(vbase + k * 16 * 128);
-      umma_bf16(tbase + 128, da, dv, idesc_bmn(128, 64), k ? 1u : 0u);
+      if (elect_one()) umma_bf16(tbase + 128, da, dv, idesc_bmn(128, 64), k ? 1u : 0u);
     }
-    umma_commit(&bars[1]);
+    if (elect_one()) umma_commit(&bars[1]);
   }
   mbar_wait(&bars[1], 1);
   tc_fence_after();

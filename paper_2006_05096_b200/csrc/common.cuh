@@ -169,6 +169,24 @@ template <int N> B2_DEV void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// ---------------------------------------------------------------- warp-uniform helpers
+// ptxas keeps TMEM addresses and UMMA descriptors in uniform registers only
+// when it can prove them warp-uniform; values derived from threadIdx or from
+// a shared-memory load are not, and every tcgen05.mma / tcgen05.ld then gets a
+// per-instruction ELECT + R2UR.BROADCAST waterfall (~100+ cycles per MMA,
+// measured: a 128x64x16 MMA stream ran at 23% tensor-pipe).  So the issuing
+// warp runs converged, derives everything from shfl-broadcast values, and
+// issues from one elected lane.
+B2_DEV int warp_index_uniform() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
+B2_DEV uint32_t uniform_u32(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
+B2_DEV bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---------------------------------------------------------------- tcgen05 / TMEM
 B2_DEV void tmem_alloc(uint32_t* smem_dst, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(

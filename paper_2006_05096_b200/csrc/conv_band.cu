@@ -1,0 +1,443 @@
+// Banded implicit-GEMM convolution on tcgen05 (sm_100a): stride-1 k x k
+// convolutions whose A operand is loaded ONCE per band of output rows and
+// reused by every filter tap through shifted shared-memory descriptors.
+//
+// The plain im2col path (gemm_tc.cu, a_im2col = 1) fetches a fresh 128 x 64
+// A tile from L2 for every (tap, channel group): a 3x3 conv streams its input
+// 9 times through the SM.  For the narrow-N layers (ResNet-50 layer1: N = 64)
+// that A stream, not the MMA, bounds the kernel.  Here a work unit is a band
+// of `bh` output rows of one image:
+//
+//   * one 4D TMA box loads the band's input rows plus halo, (bh + R - 1) rows x
+//     Wp columns x CGW channels, with out-of-bounds (the conv padding) zero
+//     filled by the TMA unit.  In shared memory the box is a matrix whose row
+//     p = hh * Wp + ww is one input pixel (CGW channels, K-major, swizzled);
+//   * output position p = oh * Wp + ow (band-local, padded-flattened) reads
+//     tap (r, s) at row p + r * Wp + s, so the UMMA A operand of tap (r, s) for
+//     M tile mt is the same matrix with its start address moved by
+//     (mt * 128 + r * Wp + s) rows — no data movement per tap;
+//   * positions with ow >= W (the Wp - W padding columns) or past the band are
+//     computed and discarded by the epilogue (<= 12.5% for ResNet/VGG shapes).
+//
+// Two A layouts:
+//   CGW = 64: 64-channel groups, 128-byte rows, SWIZZLE_128B (3x3 convs, C % 64 == 0)
+//   CGW = 16: the 16-channel space-to-depth stem tensor, 32-byte rows, SWIZZLE_32B
+// The swizzle is a function of the shared-memory address, so shifted starts
+// that stay on row boundaries see the same pattern the TMA unit wrote.
+//
+// B (weights, K-major [N][Kpad], K order (r, s, c)) is either resident — all
+// K blocks loaded once per CTA when they fit — or streamed per (tap, group)
+// through a ring.  Accumulators: MT M tiles x BN fp32 columns in TMEM, double
+// buffered so the epilogue of unit i overlaps the MMAs of unit i + 1.
+//
+// Warp roles: warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
+// warps 2..9 epilogue (two per TMEM lane quadrant, splitting columns).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace b2 {
+
+constexpr int CB_EPI_WARPS = 8;
+constexpr int CB_THREADS = (2 + CB_EPI_WARPS) * 32;
+constexpr int CB_SMEM_MAX = 232448;
+
+// SWIZZLE_32B K-major: rows of 32 B (16 bf16), 8-row atoms of 256 B
+B2_DEV uint64_t smem_desc_sw32(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;             // LBO (unused: K extent is one atom)
+  d |= (uint64_t)(256 >> 4) << 32;    // SBO: 8 rows x 32 B
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;             // SWIZZLE_32B
+  return d;
+}
+
+template <int CGW>
+B2_DEV uint64_t band_adesc(uint32_t addr) {
+  if constexpr (CGW == 64) return smem_desc_sw128(addr);
+  else return smem_desc_sw32(addr);
+}
+
+// R x S taps and B residency are compile-time so the MMA issue loop unrolls
+// to one descriptor add per operand per MMA: a single issuing thread has to
+// keep up with 64-cycle (N <= 128) / 128-cycle (N = 256) MMAs, and a loop with
+// runtime tap decomposition (integer division, parameter reloads) measured
+// ~170 cycles per MMA — the tensor pipe then idles 80% of the time.
+template <int BN, int CGW, int R, int S, bool BRES, int ACT>
+__global__ void __launch_bounds__(CB_THREADS, 1)
+    conv_band_kernel(const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB, const BandArgs a) {
+  constexpr int RB = CGW * 2;                 // bytes per A row (one pixel's channel group)
+  constexpr int KSTEPS = CGW / 16;            // UMMA K steps per tap
+  constexpr int TAPS = R * S;
+  constexpr int B_BLOCK = BN * 128;           // one 64-wide K block of weights
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + a.a_stages * a.a_stage_bytes;
+  const int nb_bufs = BRES ? a.kblocks : a.b_stages;
+  uint64_t* afull = reinterpret_cast<uint64_t*>(sB + nb_bufs * B_BLOCK);
+  uint64_t* aempty = afull + a.a_stages;
+  uint64_t* bfull = aempty + a.a_stages;
+  uint64_t* bempty = bfull + a.b_stages;
+  uint64_t* tfull = bempty + a.b_stages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bres = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
+
+  const int warp = warp_index_uniform();
+  const int lane = threadIdx.x & 31;
+  const int units = a.B * a.nbands * a.tiles_n;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.a_stages; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < a.b_stages; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], CB_EPI_WARPS);
+    }
+    mbar_init(bres, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, a.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = uniform_u32(*tmem_slot);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      if constexpr (BRES) {
+        mbar_arrive_expect_tx(bres, (uint32_t)(a.kblocks * B_BLOCK));
+        for (int kb = 0; kb < a.kblocks; ++kb) tma_load_2d(sB + kb * B_BLOCK, &tmB, bres, kb * 64, 0);
+      }
+      int as = 0, bs = 0;
+      uint32_t aph = 0, bph = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int nt = u % a.tiles_n;
+        const int rest = u / a.tiles_n;
+        const int band = rest % a.nbands;
+        const int img = rest / a.nbands;
+        for (int cg = 0; cg < a.CG; ++cg) {
+          mbar_wait(&aempty[as], aph ^ 1);
+          mbar_arrive_expect_tx(&afull[as], (uint32_t)a.a_box_bytes);
+          tma_load_4d(sA + as * a.a_stage_bytes, &tmA, &afull[as], cg * CGW, a.x0,
+                      band * a.bh + a.y0, img);
+          if (++as == a.a_stages) {
+            as = 0;
+            aph ^= 1;
+          }
+          if constexpr (!BRES) {
+            // one 64-wide K block per (tap, group): K index tap * C + cg * 64
+#pragma unroll 1
+            for (int t = 0; t < TAPS; ++t) {
+              mbar_wait(&bempty[bs], bph ^ 1);
+              mbar_arrive_expect_tx(&bfull[bs], (uint32_t)B_BLOCK);
+              tma_load_2d(sB + bs * B_BLOCK, &tmB, &bfull[bs], (t * a.CG + cg) * 64, nt * BN);
+              if (++bs == a.b_stages) {
+                bs = 0;
+                bph ^= 1;
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    // (whole warp, converged; one elected lane issues — see common.cuh)
+    constexpr uint32_t idesc = make_idesc(128, BN, 1u);
+    // per-tap A start offsets in descriptor units (16 B)
+    uint32_t toff[TAPS];
+#pragma unroll
+    for (int t = 0; t < TAPS; ++t) toff[t] = (uint32_t)(((t / S) * a.Wp + (t % S)) * RB) >> 4;
+    constexpr uint32_t MT_STEP = (128 * RB) >> 4;
+    if constexpr (BRES) {
+      mbar_wait(bres, 0);
+      tc_fence_after();
+    }
+    const uint64_t bdesc0 = smem_desc_sw128(smem_u32(sB));
+    int as = 0, bs = 0;
+    uint32_t aph = 0, bph = 0;
+    int it = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+      const int band = (u / a.tiles_n) % a.nbands;
+      const int vr = min(a.bh, a.H - band * a.bh);
+      const int mt_valid = ((vr - 1) * a.Wp + a.W - 1) / 128 + 1;
+      const int ab = it & 1;
+      mbar_wait(&tempty[ab], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t dbase = tmem_base + ab * a.MT * BN;
+      if constexpr (BRES) {
+        // CG == 1: K index of (tap t, step kk) = t * CGW + kk * 16
+        mbar_wait(&afull[as], aph);
+        tc_fence_after();
+        const uint64_t adesc0 = band_adesc<CGW>(smem_u32(sA + as * a.a_stage_bytes));
+        for (int mt = 0; mt < mt_valid; ++mt) {
+          const uint64_t adm = adesc0 + mt * MT_STEP;
+#pragma unroll
+          for (int t = 0; t < TAPS; ++t) {
+#pragma unroll
+            for (int kk = 0; kk < KSTEPS; ++kk) {
+                const int kg = t * CGW + kk * 16;
+              const uint32_t boff = (uint32_t)((kg >> 6) * B_BLOCK + ((kg >> 4) & 3) * 32) >> 4;
+              if (elect_one())
+                umma_bf16(dbase + mt * BN, adm + toff[t] + kk * 2, bdesc0 + boff, idesc,
+                          (t | kk) != 0 ? 1u : 0u);
+            }
+          }
+        }
+        if (elect_one()) umma_commit(&aempty[as]);
+        if (++as == a.a_stages) {
+          as = 0;
+          aph ^= 1;
+        }
+      } else {
+        for (int cg = 0; cg < a.CG; ++cg) {
+          mbar_wait(&afull[as], aph);
+          tc_fence_after();
+          const uint64_t adesc0 = band_adesc<CGW>(smem_u32(sA + as * a.a_stage_bytes));
+#pragma unroll
+          for (int t = 0; t < TAPS; ++t) {
+            mbar_wait(&bfull[bs], bph);
+            tc_fence_after();
+            const uint64_t bd = bdesc0 + (uint32_t)((bs * B_BLOCK) >> 4);
+            for (int mt = 0; mt < mt_valid; ++mt) {
+#pragma unroll
+              for (int kk = 0; kk < KSTEPS; ++kk)
+                if (elect_one())
+                  umma_bf16(dbase + mt * BN, adesc0 + mt * MT_STEP + toff[t] + kk * 2,
+                            bd + kk * 2, idesc, (cg | t | kk) != 0 ? 1u : 0u);
+            }
+            if (elect_one()) umma_commit(&bempty[bs]);
+            if (++bs == a.b_stages) {
+              bs = 0;
+              bph ^= 1;
+            }
+          }
+          if (elect_one()) umma_commit(&aempty[as]);
+          if (++as == a.a_stages) {
+            as = 0;
+            aph ^= 1;
+          }
+        }
+      }
+      if (elect_one()) umma_commit(&tfull[ab]);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;                 // TMEM lane quadrant
+    const int eh = (warp - 2) >> 2;         // column half
+    int it = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+      const int nt = u % a.tiles_n;
+      const int rest = u / a.tiles_n;
+      const int band = rest % a.nbands;
+      const int img = rest / a.nbands;
+      const int vr = min(a.bh, a.H - band * a.bh);
+      const int mt_valid = ((vr - 1) * a.Wp + a.W - 1) / 128 + 1;
+      const int n0 = nt * BN;
+      const int ab = it & 1;
+      mbar_wait(&tfull[ab], (it >> 1) & 1);
+      tc_fence_after();
+      for (int mt = 0; mt < mt_valid; ++mt) {
+        const int p = mt * 128 + q * 32 + lane;
+        const int oh = p / a.Wp;
+        const int ow = p - oh * a.Wp;
+        const bool valid = ow < a.W && oh < vr;
+        bf16* orow = a.out + ((size_t)(img * a.H + band * a.bh + oh) * a.W + ow) * a.N + n0;
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + ab * a.MT * BN + mt * BN;
+#pragma unroll 1
+        for (int c = eh * 32; c < BN; c += 64) {
+          uint32_t rr[32];
+          tmem_ld_32x32b_x32(taddr + c, rr);
+          float bv[32];
+          const float4* bp = reinterpret_cast<const float4*>(a.bias + n0 + c);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 b4 = __ldg(bp + j);
+            bv[4 * j] = b4.x;
+            bv[4 * j + 1] = b4.y;
+            bv[4 * j + 2] = b4.z;
+            bv[4 * j + 3] = b4.w;
+          }
+          tmem_wait_ld();
+          if (valid) {
+            uint4* op = reinterpret_cast<uint4*>(orow + c);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float v[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                v[e] = act_t<ACT>(__uint_as_float(rr[8 * j + e]) + bv[8 * j + e]);
+              uint4 w;
+              w.x = pack_bf16x2(v[0], v[1]);
+              w.y = pack_bf16x2(v[2], v[3]);
+              w.z = pack_bf16x2(v[4], v[5]);
+              w.w = pack_bf16x2(v[6], v[7]);
+              op[j] = w;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[ab]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, a.tmem_cols);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+int band_smem_bytes(const BandArgs& a, int bn) {
+  const int nb = a.b_resident ? a.kblocks : a.b_stages;
+  return 1024 + a.a_stages * a.a_stage_bytes + nb * bn * 128 +
+         8 * (2 * a.a_stages + 2 * a.b_stages + 5) + 16;
+}
+
+// Fill the A-stage geometry of `a` for a band of `bh` rows.
+static void band_geometry(BandArgs& a, int bh, int bn, int rb) {
+  a.bh = bh;
+  a.nbands = (a.H + bh - 1) / bh;
+  a.MT = ((bh - 1) * a.Wp + a.W - 1) / 128 + 1;
+  const int box_rows = (bh + a.R - 1) * a.Wp;
+  const int need_rows = a.MT * 128 + (a.R - 1) * a.Wp + (a.S - 1);
+  const int rows = ((box_rows > need_rows ? box_rows : need_rows) + 7) / 8 * 8;
+  a.a_box_bytes = box_rows * rb;
+  a.a_stage_bytes = (rows * rb + 1023) / 1024 * 1024;
+  const int tmem = 2 * a.MT * bn;
+  a.tmem_cols = tmem <= 32 ? 32 : tmem <= 64 ? 64 : tmem <= 128 ? 128 : tmem <= 256 ? 256 : 512;
+}
+
+// Choose band height (M tiles per band), pipeline depths and B residency.
+// Candidates are ranked by the fraction of computed positions that are real
+// outputs, then by B residency (no per-unit weight traffic), then by band
+// size (less halo re-read).  Returns false when nothing fits (the caller
+// keeps the im2col path).
+bool band_config(BandArgs& a, int bn, int cgw, int mt_cap) {
+  const int rb = cgw * 2;
+  const int max_mt = 512 / (2 * bn);          // double-buffered accumulators in 512 TMEM cols
+  if (max_mt < 1 || a.Wp > 256) return false;
+  struct Cand { int bh, res, ast, bst; double eff; };
+  Cand best{0, 0, 0, 0, 0.0};
+  for (int mt = 1; mt <= max_mt && mt <= mt_cap; ++mt) {
+    int bh = (mt * 128) / a.Wp;
+    if (bh < 1) continue;
+    if (bh > a.H) bh = a.H;
+    const int bands = (a.H + bh - 1) / bh;
+    double computed = 0.0;
+    for (int b = 0; b < bands; ++b) {
+      const int vr = (a.H - b * bh) < bh ? (a.H - b * bh) : bh;
+      computed += (double)(((vr - 1) * a.Wp + a.W - 1) / 128 + 1) * 128;
+    }
+    Cand c{bh, 0, 0, 0, (double)a.H * a.W / computed};
+    BandArgs t = a;
+    band_geometry(t, bh, bn, rb);
+    if (t.MT * 2 * bn > 512) continue;
+    t.b_resident = 1;
+    t.b_stages = 0;
+    t.a_stages = 2;
+    const bool res_ok = a.tiles_n == 1 && a.CG == 1 && bn == 64;   // instantiated resident kernels
+    if (res_ok && band_smem_bytes(t, bn) <= CB_SMEM_MAX) {
+      c.res = 1;
+      c.ast = (a.CG > 1 && (t.a_stages = 3, band_smem_bytes(t, bn) <= CB_SMEM_MAX)) ? 3 : 2;
+    } else if (cgw == 64) {   // streamed B needs one (tap, group) per K block
+      t.b_resident = 0;
+      for (int ast = 3; ast >= 2 && !c.ast; --ast)
+        for (int bst = 6; bst >= 3 && !c.ast; --bst) {
+          t.a_stages = ast;
+          t.b_stages = bst;
+          if (band_smem_bytes(t, bn) <= CB_SMEM_MAX) {
+            c.ast = ast;
+            c.bst = bst;
+          }
+        }
+    }
+    if (!c.ast) continue;
+    const bool better = !best.bh || c.eff > best.eff + 0.02 ||
+                        (c.eff > best.eff - 0.02 && (c.res > best.res ||
+                                                     (c.res == best.res && c.bh > best.bh)));
+    if (better) best = c;
+  }
+  if (!best.bh) return false;
+  band_geometry(a, best.bh, bn, rb);
+  a.b_resident = best.res;
+  a.a_stages = best.ast;
+  a.b_stages = best.bst;
+  return band_smem_bytes(a, bn) <= CB_SMEM_MAX;
+}
+
+template <int BN, int CGW, int R, int S, bool BRES, int ACT>
+static cudaError_t band_launch_t(const BandArgs& a, const CUtensorMap& ta, const CUtensorMap& tb,
+                                 int num_sms, cudaStream_t st) {
+  auto kern = conv_band_kernel<BN, CGW, R, S, BRES, ACT>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         CB_SMEM_MAX);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int units = a.B * a.nbands * a.tiles_n;
+  const int grid = units < num_sms ? units : num_sms;
+  kern<<<grid, CB_THREADS, band_smem_bytes(a, BN), st>>>(ta, tb, a);
+  return cudaGetLastError();
+}
+
+template <int ACT>
+static cudaError_t band_dispatch(const BandArgs& a, int bn, int cgw, const CUtensorMap& ta,
+                                 const CUtensorMap& tb, int num_sms, cudaStream_t st) {
+  if (cgw == 16) {   // space-to-depth 7x7/2 stem: 4 x 4 taps, resident weights
+    if (bn == 64 && a.R == 4 && a.S == 4 && a.b_resident && a.CG == 1)
+      return band_launch_t<64, 16, 4, 4, true, ACT>(a, ta, tb, num_sms, st);
+    return cudaErrorInvalidValue;
+  }
+  if (a.R != 3 || a.S != 3) return cudaErrorInvalidValue;
+  if (a.b_resident) {
+    if (bn == 64 && a.CG == 1) return band_launch_t<64, 64, 3, 3, true, ACT>(a, ta, tb, num_sms, st);
+    return cudaErrorInvalidValue;
+  }
+  switch (bn) {
+    case 64: return band_launch_t<64, 64, 3, 3, false, ACT>(a, ta, tb, num_sms, st);
+    case 128: return band_launch_t<128, 64, 3, 3, false, ACT>(a, ta, tb, num_sms, st);
+    case 256: return band_launch_t<256, 64, 3, 3, false, ACT>(a, ta, tb, num_sms, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// Which (taps, BN, residency) combinations have a kernel instance.
+bool band_supported(const BandArgs& a, int bn, int cgw, int act) {
+  if (act != ACT_NONE && act != ACT_RELU) return false;
+  if (cgw == 16) return bn == 64 && a.R == 4 && a.S == 4 && a.b_resident && a.CG == 1;
+  if (a.R != 3 || a.S != 3) return false;
+  if (a.b_resident) return bn == 64 && a.CG == 1;
+  return bn == 64 || bn == 128 || bn == 256;
+}
+
+cudaError_t conv_band_launch(const BandArgs& a, int bn, int cgw, const CUtensorMap& ta,
+                             const CUtensorMap& tb, int num_sms, cudaStream_t st) {
+  if (a.act == ACT_RELU) return band_dispatch<ACT_RELU>(a, bn, cgw, ta, tb, num_sms, st);
+  if (a.act == ACT_NONE) return band_dispatch<ACT_NONE>(a, bn, cgw, ta, tb, num_sms, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace b2

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = warp_index_uniform();
   const int lane = threadIdx.x & 31;
   const int ntiles = a.tiles_m * a.tiles_n;
 
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = uniform_u32(*tmem_slot);
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -293,7 +293,8 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // (whole warp, converged; one elected lane issues — see common.cuh)
+    {
       constexpr uint32_t idesc = make_idesc(TC_BM, BN, 1u);
       int stage = 0;
       uint32_t phase = 0;
@@ -315,14 +316,14 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
           const uint64_t bd = smem_desc_sw128(smem_u32(sB + stage * Cfg::B_BYTES));
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k)
-            umma_bf16(dt, ad + astep * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
-          umma_commit(&empty[stage]);
+            if (elect_one()) umma_bf16(dt, ad + astep * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          if (elect_one()) umma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[as]);
+        if (elect_one()) umma_commit(&tfull[as]);
       }
     }
   } else if (warp < 2 + TC_EPI_WARPS) {

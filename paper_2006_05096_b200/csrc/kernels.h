@@ -43,6 +43,27 @@ struct TcArgs {
                         // BN/64 extra K blocks per tile, A from tmR, B from the identity
 };
 
+// ---- banded implicit-GEMM conv (conv_band.cu) --------------------------------
+struct BandArgs {
+  int B, H, W, N;       // output NHWC [B, H, W, N]
+  int Wp;               // A view row pitch in pixels (W + S - 1, or the s2d width)
+  int R, S;             // taps; tap (r, s) reads A row p + r * Wp + s
+  int CG;               // channel groups per tap (C / 64; 1 for the s2d stem)
+  int x0, y0;           // A box start offsets (-pad for zero-filled halos)
+  int kblocks;          // Kpad / 64 (weight K blocks)
+  int tiles_n;          // N / BN
+  // geometry chosen by band_config
+  int bh, nbands, MT;
+  int a_box_bytes, a_stage_bytes, a_stages, b_stages, b_resident, tmem_cols;
+  const float* bias;
+  bf16* out;
+  int act;
+};
+bool band_config(BandArgs& a, int bn, int cgw, int mt_cap = 4);
+bool band_supported(const BandArgs& a, int bn, int cgw, int act);
+cudaError_t conv_band_launch(const BandArgs& a, int bn, int cgw, const CUtensorMap& ta,
+                             const CUtensorMap& tb, int num_sms, cudaStream_t st);
+
 int tc_pick_bn(long M, int N, int num_sms);
 cudaError_t tc_gemm_launch(const TcArgs& a, int bn, bool gather, const CUtensorMap& ta,
                            const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& tr,

@@ -201,6 +201,8 @@ struct BatchState {
   std::vector<CUtensorMap> tmR;    // per layer (tc, residual fold): residual as an A operand
   std::vector<char> fold;          // per layer: residual folded into the MMA
   std::vector<CUtensorMap> tmI;    // per layer: identity [256 x 256] (box rows = BN) for the fold
+  std::vector<char> band;          // per layer: banded implicit-GEMM conv (conv_band.cu)
+  std::vector<BandArgs> bargs;     // per layer (band): geometry chosen by band_config
   cudaGraphExec_t graph = nullptr;
   void* h_in = nullptr;            // pinned (e2e)
   void* h_out = nullptr;
@@ -231,7 +233,10 @@ struct b2_plan {
   bool use_s2d = true;       // B2_S2D=0 -> stems on the cp.async gather path
   bool im2col8 = false;      // B2_IM2COL8=1 -> 8-channel-tap im2col TMA for C == 8 stems
                              // (correct, but issue-bound on 2 KB boxes: slower than gather)
+  bool use_band = true;      // B2_BAND=0 -> stride-1 k x k convs and s2d stems on gemm_tc
+  int band_max_n = 128;      // B2_BAND_MAX_N: widest conv (output channels) sent to conv_band
   void* identity = nullptr;  // bf16 I[256][256]
+  float* zero_bias = nullptr;  // fp32 zeros[8192]: bias of bias-free layers in fused epilogues
   int stages_override = 0;   // B2_STAGES
 };
 
@@ -520,7 +525,10 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
         const int res_t = conv ? p[15] : p[8];
         const int act = conv ? p[14] : p[7];
         T* out = A(p[1]);
-        if (L.tc) {
+        if (L.tc && S.band[li]) {
+          CK(conv_band_launch(S.bargs[li], S.bn[li], L.s2d ? 16 : 64, S.tmA[li], S.tmB[li],
+                              pl->num_sms, st));
+        } else if (L.tc) {
           TcArgs a{};
           a.M = (int)M;
           a.N = N;
@@ -662,6 +670,77 @@ size_t in_bytes(const b2_plan* pl, int batch) {
   return (size_t)batch * pl->in_elems * (pl->input_kind == B2_IN_TOKENS_I64 ? 8 : 4);
 }
 
+// Banded implicit-GEMM conv (conv_band.cu) for stride-1 "same" k x k convs
+// with C % 64 == 0 and for space-to-depth stems.  Returns 1 when layer li
+// runs banded (tensor maps built), 0 to keep the gemm_tc path, -code on error.
+int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
+  Layer& L = pl->layers[li];
+  const int* p = L.p;
+  if (!pl->use_band || L.kind != OP_CONV || p[15] >= 0) return 0;
+  const int C = p[6], N = p[7], R = p[8], Sf = p[9], stride = p[10], pad = p[11];
+  const int OH = p[12], OW = p[13];
+  BandArgs a{};
+  int cgw = 64;
+  if (L.s2d) {
+    if (N % 64 != 0 || N > 128) return 0;
+    cgw = 16;
+    a.Wp = L.s2d_W2;
+    a.R = a.S = L.s2d_Rp;
+    a.CG = 1;
+    a.x0 = a.y0 = 0;
+  } else {
+    // N >= 256: the im2col GEMM's wide tiles already amortise A (measured:
+    // band 62.8 / 108 us vs im2col 60.8 / 99.7 us on ResNet layer3 / layer4)
+    if (N > pl->band_max_n) return 0;
+    if (!L.im2col || stride != 1 || R != Sf || (R & 1) == 0 || pad != (R - 1) / 2 ||
+        OH != p[4] || OW != p[5] || C % 64 != 0 || N % 64 != 0 || R == 1)
+      return 0;
+    a.Wp = OW + Sf - 1;
+    a.R = R;
+    a.S = Sf;
+    a.CG = C / 64;
+    a.x0 = a.y0 = -pad;
+  }
+  const int bn = N % 256 == 0 ? 256 : N % 128 == 0 ? 128 : 64;
+  if (cgw == 16 && bn > 128) return 0;
+  a.B = batch;
+  a.H = OH;
+  a.W = OW;
+  a.N = N;
+  a.kblocks = L.kpad / 64;
+  a.tiles_n = N / bn;
+  a.out = reinterpret_cast<bf16*>(S.act[p[1]]);
+  a.act = p[14];
+  a.bias = L.bias ? L.bias : pl->zero_bias;
+  if (!band_config(a, bn, cgw) || !band_supported(a, bn, cgw, a.act)) return 0;
+  if ((long)a.B * a.nbands * a.tiles_n < pl->num_sms) {   // small batch: more, smaller units
+    BandArgs t = a;
+    if (band_config(t, bn, cgw, 1) && band_supported(t, bn, cgw, t.act)) a = t;
+  }
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return -fail(B2_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int cin = L.s2d ? 16 : C;
+  const int win = L.s2d ? L.s2d_W2 : p[5];
+  const int hin = L.s2d ? L.s2d_H2 : p[4];
+  cuuint64_t dims[4] = {(cuuint64_t)cin, (cuuint64_t)win, (cuuint64_t)hin, (cuuint64_t)batch};
+  cuuint64_t str[3] = {(cuuint64_t)cin * 2, (cuuint64_t)win * cin * 2,
+                       (cuuint64_t)hin * win * cin * 2};
+  cuuint32_t box[4] = {(cuuint32_t)cgw, (cuuint32_t)a.Wp, (cuuint32_t)(a.bh + a.R - 1), 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  if (fn(&S.tmA[li], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, S.act[p[0]], dims, str, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE,
+         cgw == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -fail(B2_ERR_CUDA, "layer %zu: band A tensor map rejected", li);
+  if (!make_tmap_bf16(&S.tmB[li], L.w, (uint64_t)N, (uint64_t)L.kpad, (uint64_t)L.kpad * 2,
+                      (uint32_t)bn))
+    return -fail(B2_ERR_CUDA, "layer %zu: band B tensor map rejected", li);
+  S.bn[li] = bn;
+  S.band[li] = 1;
+  S.bargs[li] = a;
+  return 1;
+}
+
 int get_state(b2_plan* pl, int batch, BatchState** out) {
   auto it = pl->states.find(batch);
   if (it != pl->states.end()) {
@@ -689,10 +768,15 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
   S.tmR.resize(pl->layers.size());
   S.fold.assign(pl->layers.size(), 0);
   S.tmI.resize(pl->layers.size());
+  S.band.assign(pl->layers.size(), 0);
+  S.bargs.resize(pl->layers.size());
   for (size_t li = 0; li < pl->layers.size(); ++li) {
     Layer& L = pl->layers[li];
     if (!L.tc) continue;
     const int* p = L.p;
+    int brc = plan_band(pl, S, li, batch);
+    if (brc < 0) return -brc;
+    if (brc == 1) continue;
     if (L.kind == OP_ATTENTION) {
       const uint64_t cols = 3ull * p[2] * p[3];
       if (!make_tmap_bf16(&S.tmA[li], S.act[p[0]], (uint64_t)batch * p[4], cols, cols * 2, 128))
@@ -848,6 +932,8 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* ic = getenv("B2_IM2COL")) pl->use_im2col = ic[0] != '0';
   if (const char* i8 = getenv("B2_IM2COL8")) pl->im2col8 = i8[0] == '1';
   if (const char* sd = getenv("B2_S2D")) pl->use_s2d = sd[0] != '0';
+  if (const char* bd = getenv("B2_BAND")) pl->use_band = bd[0] != '0';
+  if (const char* bm = getenv("B2_BAND_MAX_N")) pl->band_max_n = atoi(bm);
   cudaGetDevice(&pl->device);
   cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, pl->device);
   int major = 0;
@@ -884,6 +970,10 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
     std::vector<float> eye(256 * 256, 0.f);
     for (int i = 0; i < 256; ++i) eye[i * 256 + i] = 1.f;
     rc = upload_as<bf16>(pl, eye, &pl->identity);
+    if (!rc) {
+      std::vector<float> z(8192, 0.f);
+      rc = upload_f32(pl, z.data(), z.size(), &pl->zero_bias);
+    }
   }
   if (!rc) {
     // algorithmic FLOPs (2 per MAC) of the contraction ops

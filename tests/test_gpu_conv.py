@@ -1,0 +1,87 @@
+"""Per-shape conv parity on the GPU: single-conv plans through every tcgen05
+conv path (banded implicit GEMM with resident or streamed weights and 1..4 M
+tiles per band, the TMA-im2col GEMM, the space-to-depth stem) checked
+layerwise against the numpy oracle (plan_ref.conv2d_nhwc on the bf16-rounded
+operands, fp64 accumulation).  Tolerance: 1e-2 normwise = one bf16 rounding
+of the op output (same bound as tests/test_gpu.py's layerwise gate).
+
+Batch sizes are chosen so both the small-batch (one M tile per band) and the
+large-batch (multi-tile bands) configurations run for each shape.
+"""
+import numpy as np
+import pytest
+
+import plan_ref
+from paper_2006_05096_b200 import plan as P
+from paper_2006_05096_b200 import runtime as R
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2
+
+
+def conv_plan(H, W, C, N, k, stride, act=1, seed=0):
+    pad = k // 2
+    OH = (H + 2 * pad - k) // stride + 1
+    OW = (W + 2 * pad - k) // stride + 1
+    b = P.PlanBuilder("conv")
+    Cp = max(8, C)
+    x = b.tensor(H, W, Cp)
+    b.in_elems = C * H * W
+    b.op_p(P.OP_INPUT, [x, C, H, W, Cp])
+    rng = np.random.default_rng(seed)
+    y = b.tensor(OH, OW, N)
+    w = rng.standard_normal((N, k, k, Cp)) * (1.0 / np.sqrt(k * k * C))
+    w[..., C:] = 0.0
+    bias = rng.standard_normal(N) * 0.1
+    b.op_p(P.OP_CONV, [x, y, b.weight(w), b.weight(bias), H, W, Cp, N, k, k, stride, pad,
+                       OH, OW, act, -1])
+    b.out_elems = b.tensors[y].elems
+    b.op_p(P.OP_OUTPUT, [1, y, 0])
+    return b.build(P.DT_FP32)
+
+
+def check(blob, batch, seed=3):
+    pl = P.decode(blob)
+    x = plan_ref.make_inputs(pl, batch, seed)
+    plan = R.Plan(blob, P.DT_BF16)
+    try:
+        out = plan.predict(x)
+        assert np.isfinite(out).all()
+        rt = lambda t: plan.read_tensor(batch, t, pl.tensors[t].elems, pl.tensors[t].kind)
+        errs = plan_ref.layerwise_errors(pl, rt, x, True)
+        bad = [e for e in errs if not e[2] <= TOL]
+        assert not bad, bad
+    finally:
+        plan.close()
+
+
+@pytest.mark.parametrize("H,W,C,N,batch", [
+    (56, 56, 64, 64, 1),      # layer1 3x3, small batch (1 tile per band)
+    (56, 56, 64, 64, 16),     # layer1 3x3, multi-tile bands, resident weights
+    (28, 28, 128, 128, 2),
+    (28, 28, 128, 128, 24),   # layer2 3x3: two channel groups
+    (14, 14, 256, 256, 12),   # layer3 3x3: BN = 256
+    (7, 7, 512, 512, 32),     # layer4 3x3: two N tiles, streamed weights
+    (112, 112, 64, 128, 2),   # VGG block 2
+    (224, 224, 64, 64, 1),    # VGG block 1: a row spans two M tiles
+    (20, 36, 64, 192, 5),     # ragged: N = 3 x 64, partial last band
+])
+def test_conv3x3(gpu_required, monkeypatch, H, W, C, N, batch):
+    monkeypatch.setenv("B2_BAND_MAX_N", "4096")   # every shape through the band kernel
+    check(conv_plan(H, W, C, N, 3, 1), batch)
+    monkeypatch.setenv("B2_BAND", "0")            # and through the im2col GEMM
+    check(conv_plan(H, W, C, N, 3, 1), batch)
+
+
+@pytest.mark.parametrize("batch", [1, 2, 16])
+def test_stem_s2d(gpu_required, batch):
+    """7x7/2 stem on 3 channels: the space-to-depth band path (16-ch, 32B swizzle)."""
+    check(conv_plan(224, 224, 3, 64, 7, 2), batch)
+
+
+@pytest.mark.parametrize("k,stride,H,C,N", [(3, 2, 28, 128, 128), (1, 2, 28, 256, 512),
+                                             (5, 1, 14, 64, 64)])
+def test_other_convs(gpu_required, k, stride, H, C, N):
+    """Strided / 5x5 convs: band path for stride 1 k x k, im2col GEMM otherwise."""
+    check(conv_plan(H, H, C, N, k, stride), 4)
