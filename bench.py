@@ -6,7 +6,8 @@ at batch 256 (BASELINE.json configs[1], the largest single-GPU profile cell),
 replayed from a CUDA graph inside libb2 with inputs resident in HBM, timed
 with CUDA events (``b2_bench``).  ``e2e`` is the same metric through the
 C-ABI call with HOST buffers (``b2_bench_e2e``: pinned H2D of the fp32 input
-batch, forward, D2H of the logits, every step).
+batch, forward, D2H of the logits, every step; the copies of neighbouring steps
+overlap the forward on separate streams, as a serving pipeline would).
 
 Multi-GPU (torchrun): one process per GPU, each runs its own replica of the
 step (the sweep shards by cell with no data-path collective: "scaling": weak);
@@ -226,7 +227,10 @@ def run_ours(args) -> dict | None:
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT,
                 "h2d_bytes_per_step": int(B * plan.in_elems * 4),
                 "d2h_bytes_per_step": int(B * plan.out_elems * 4),
-                "ms_per_step": round(e2e_ms / K, 4)},
+                "ms_per_step": round(e2e_ms / K, 4),
+                "p50_ms": round(float(np.percentile(elat, 50)), 4),
+                "mode": "b2_bench_e2e: pinned fp32 inputs H2D + forward + logits D2H every step, "
+                        "software-pipelined over 3 streams (H2D i+1 and D2H i-1 overlap forward i)"},
         "gpu_launches": int(K * plan.launches_per_forward),
         "clocks": clk.summary(),
     }

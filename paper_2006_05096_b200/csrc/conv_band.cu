@@ -40,6 +40,7 @@ namespace b2 {
 constexpr int CB_EPI_WARPS = 8;
 constexpr int CB_THREADS = (2 + CB_EPI_WARPS) * 32;
 constexpr int CB_SMEM_MAX = 232448;
+constexpr int CB_EPI_BYTES = CB_EPI_WARPS * 2 * 2048;   // per-warp double-buffered 32 x 64 B tiles
 
 // SWIZZLE_32B K-major: rows of 32 B (16 bf16), 8-row atoms of 256 B
 B2_DEV uint64_t smem_desc_sw32(uint32_t smem_addr) {
@@ -66,7 +67,8 @@ B2_DEV uint64_t band_adesc(uint32_t addr) {
 template <int BN, int CGW, int R, int S, bool BRES, int ACT>
 __global__ void __launch_bounds__(CB_THREADS, 1)
     conv_band_kernel(const __grid_constant__ CUtensorMap tmA,
-                     const __grid_constant__ CUtensorMap tmB, const BandArgs a) {
+                     const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmO, const BandArgs a) {
   constexpr int RB = CGW * 2;                 // bytes per A row (one pixel's channel group)
   constexpr int KSTEPS = CGW / 16;            // UMMA K steps per tap
   constexpr int TAPS = R * S;
@@ -77,7 +79,8 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
   uint8_t* sA = smem;
   uint8_t* sB = sA + a.a_stages * a.a_stage_bytes;
   const int nb_bufs = BRES ? a.kblocks : a.b_stages;
-  uint64_t* afull = reinterpret_cast<uint64_t*>(sB + nb_bufs * B_BLOCK);
+  uint8_t* sEpi = sB + nb_bufs * B_BLOCK;     // 8 warps x 2 staging tiles of 32 x 64 B
+  uint64_t* afull = reinterpret_cast<uint64_t*>(sEpi + CB_EPI_BYTES);
   uint64_t* aempty = afull + a.a_stages;
   uint64_t* bfull = aempty + a.a_stages;
   uint64_t* bempty = bfull + a.b_stages;
@@ -109,6 +112,7 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmO);
   }
   if (warp == 1) tmem_alloc(tmem_slot, a.tmem_cols);
   tc_fence_before();
@@ -238,8 +242,18 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
+    // TMEM -> registers (+bias, act) -> bf16 -> 64B-swizzled 32 x 32 staging
+    // tile -> TMA store.  The 4D output map [N, W, H, B] clips the padding
+    // columns (ow >= W) in hardware; rows past the band's valid rows are
+    // skipped so neighbouring bands are never overwritten.
     const int q = warp & 3;                 // TMEM lane quadrant
-    const int eh = (warp - 2) >> 2;         // column half
+    const int ew = warp - 2;
+    const int eh = ew >> 2;                 // column half
+    uint8_t* obuf = sEpi + ew * 4096;
+    uint32_t oi = 0;
+    const uint32_t swz = (lane >> 1) & 3;
+    float bpre[32];
+    int bpre_n0 = -1;
     int it = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
       const int nt = u % a.tiles_n;
@@ -250,52 +264,88 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
       const int mt_valid = ((vr - 1) * a.Wp + a.W - 1) / 128 + 1;
       const int n0 = nt * BN;
       const int ab = it & 1;
+      if constexpr (BN == 64) {   // one 32-column chunk per warp: bias lives in registers
+        if (n0 != bpre_n0) {
+          const float4* bp = reinterpret_cast<const float4*>(a.bias + n0 + eh * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 b4 = __ldg(bp + j);
+            bpre[4 * j] = b4.x;
+            bpre[4 * j + 1] = b4.y;
+            bpre[4 * j + 2] = b4.z;
+            bpre[4 * j + 3] = b4.w;
+          }
+          bpre_n0 = n0;
+        }
+      }
       mbar_wait(&tfull[ab], (it >> 1) & 1);
       tc_fence_after();
       for (int mt = 0; mt < mt_valid; ++mt) {
-        const int p = mt * 128 + q * 32 + lane;
-        const int oh = p / a.Wp;
-        const int ow = p - oh * a.Wp;
-        const bool valid = ow < a.W && oh < vr;
-        bf16* orow = a.out + ((size_t)(img * a.H + band * a.bh + oh) * a.W + ow) * a.N + n0;
+        const int p0 = mt * 128 + q * 32;               // band position of lane 0
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + ab * a.MT * BN + mt * BN;
 #pragma unroll 1
         for (int c = eh * 32; c < BN; c += 64) {
           uint32_t rr[32];
           tmem_ld_32x32b_x32(taddr + c, rr);
           float bv[32];
-          const float4* bp = reinterpret_cast<const float4*>(a.bias + n0 + c);
+          if constexpr (BN == 64) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float4 b4 = __ldg(bp + j);
-            bv[4 * j] = b4.x;
-            bv[4 * j + 1] = b4.y;
-            bv[4 * j + 2] = b4.z;
-            bv[4 * j + 3] = b4.w;
-          }
-          tmem_wait_ld();
-          if (valid) {
-            uint4* op = reinterpret_cast<uint4*>(orow + c);
+            for (int j = 0; j < 32; ++j) bv[j] = bpre[j];
+          } else {
+            const float4* bp = reinterpret_cast<const float4*>(a.bias + n0 + c);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              float v[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e)
-                v[e] = act_t<ACT>(__uint_as_float(rr[8 * j + e]) + bv[8 * j + e]);
-              uint4 w;
-              w.x = pack_bf16x2(v[0], v[1]);
-              w.y = pack_bf16x2(v[2], v[3]);
-              w.z = pack_bf16x2(v[4], v[5]);
-              w.w = pack_bf16x2(v[6], v[7]);
-              op[j] = w;
+            for (int j = 0; j < 8; ++j) {
+              const float4 b4 = __ldg(bp + j);
+              bv[4 * j] = b4.x;
+              bv[4 * j + 1] = b4.y;
+              bv[4 * j + 2] = b4.z;
+              bv[4 * j + 3] = b4.w;
             }
           }
+          tmem_wait_ld();
+          if (lane == 0) bulk_wait_read<1>();          // staging buffer (oi & 1) free again
+          __syncwarp();
+          uint8_t* orow = obuf + (oi & 1) * 2048 + lane * 64;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              v[e] = act_t<ACT>(__uint_as_float(rr[8 * j + e]) + bv[8 * j + e]);
+            uint4 w;
+            w.x = pack_bf16x2(v[0], v[1]);
+            w.y = pack_bf16x2(v[2], v[3]);
+            w.z = pack_bf16x2(v[4], v[5]);
+            w.w = pack_bf16x2(v[6], v[7]);
+            *reinterpret_cast<uint4*>(orow + ((j ^ swz) << 4)) = w;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            // Wp is a multiple of 32 (a chunk lies in one output row; columns
+            // >= W clip) or divides 32 (a chunk holds 32 / Wp whole rows; each
+            // row's store starts at a 512 B-aligned staging offset).  TMA
+            // stores reject negative coordinates, hence this geometry.
+            const uint8_t* src = obuf + (oi & 1) * 2048;
+            if (a.Wp >= 32) {
+              const int r = p0 / a.Wp;
+              if (r < vr) tma_store_4d(&tmO, src, n0 + c, p0 - r * a.Wp, band * a.bh + r, img);
+            } else {
+              for (int j = 0; j < 32 / a.Wp; ++j) {
+                const int r = p0 / a.Wp + j;
+                if (r < vr) tma_store_4d(&tmO, src + j * a.Wp * 64, n0 + c, 0, band * a.bh + r, img);
+              }
+            }
+            bulk_commit();
+          }
+          ++oi;
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
     }
+    if (lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
@@ -310,7 +360,7 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
 
 int band_smem_bytes(const BandArgs& a, int bn) {
   const int nb = a.b_resident ? a.kblocks : a.b_stages;
-  return 1024 + a.a_stages * a.a_stage_bytes + nb * bn * 128 +
+  return 1024 + a.a_stages * a.a_stage_bytes + nb * bn * 128 + CB_EPI_BYTES +
          8 * (2 * a.a_stages + 2 * a.b_stages + 5) + 16;
 }
 
@@ -388,7 +438,7 @@ bool band_config(BandArgs& a, int bn, int cgw, int mt_cap) {
 
 template <int BN, int CGW, int R, int S, bool BRES, int ACT>
 static cudaError_t band_launch_t(const BandArgs& a, const CUtensorMap& ta, const CUtensorMap& tb,
-                                 int num_sms, cudaStream_t st) {
+                                 const CUtensorMap& to, int num_sms, cudaStream_t st) {
   auto kern = conv_band_kernel<BN, CGW, R, S, BRES, ACT>;
   static bool configured = false;
   if (!configured) {
@@ -399,27 +449,28 @@ static cudaError_t band_launch_t(const BandArgs& a, const CUtensorMap& ta, const
   }
   const int units = a.B * a.nbands * a.tiles_n;
   const int grid = units < num_sms ? units : num_sms;
-  kern<<<grid, CB_THREADS, band_smem_bytes(a, BN), st>>>(ta, tb, a);
+  kern<<<grid, CB_THREADS, band_smem_bytes(a, BN), st>>>(ta, tb, to, a);
   return cudaGetLastError();
 }
 
 template <int ACT>
 static cudaError_t band_dispatch(const BandArgs& a, int bn, int cgw, const CUtensorMap& ta,
-                                 const CUtensorMap& tb, int num_sms, cudaStream_t st) {
+                                 const CUtensorMap& tb, const CUtensorMap& to, int num_sms,
+                                 cudaStream_t st) {
   if (cgw == 16) {   // space-to-depth 7x7/2 stem: 4 x 4 taps, resident weights
     if (bn == 64 && a.R == 4 && a.S == 4 && a.b_resident && a.CG == 1)
-      return band_launch_t<64, 16, 4, 4, true, ACT>(a, ta, tb, num_sms, st);
+      return band_launch_t<64, 16, 4, 4, true, ACT>(a, ta, tb, to, num_sms, st);
     return cudaErrorInvalidValue;
   }
   if (a.R != 3 || a.S != 3) return cudaErrorInvalidValue;
   if (a.b_resident) {
-    if (bn == 64 && a.CG == 1) return band_launch_t<64, 64, 3, 3, true, ACT>(a, ta, tb, num_sms, st);
+    if (bn == 64 && a.CG == 1) return band_launch_t<64, 64, 3, 3, true, ACT>(a, ta, tb, to, num_sms, st);
     return cudaErrorInvalidValue;
   }
   switch (bn) {
-    case 64: return band_launch_t<64, 64, 3, 3, false, ACT>(a, ta, tb, num_sms, st);
-    case 128: return band_launch_t<128, 64, 3, 3, false, ACT>(a, ta, tb, num_sms, st);
-    case 256: return band_launch_t<256, 64, 3, 3, false, ACT>(a, ta, tb, num_sms, st);
+    case 64: return band_launch_t<64, 64, 3, 3, false, ACT>(a, ta, tb, to, num_sms, st);
+    case 128: return band_launch_t<128, 64, 3, 3, false, ACT>(a, ta, tb, to, num_sms, st);
+    case 256: return band_launch_t<256, 64, 3, 3, false, ACT>(a, ta, tb, to, num_sms, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -434,9 +485,10 @@ bool band_supported(const BandArgs& a, int bn, int cgw, int act) {
 }
 
 cudaError_t conv_band_launch(const BandArgs& a, int bn, int cgw, const CUtensorMap& ta,
-                             const CUtensorMap& tb, int num_sms, cudaStream_t st) {
-  if (a.act == ACT_RELU) return band_dispatch<ACT_RELU>(a, bn, cgw, ta, tb, num_sms, st);
-  if (a.act == ACT_NONE) return band_dispatch<ACT_NONE>(a, bn, cgw, ta, tb, num_sms, st);
+                             const CUtensorMap& tb, const CUtensorMap& to, int num_sms,
+                             cudaStream_t st) {
+  if (a.act == ACT_RELU) return band_dispatch<ACT_RELU>(a, bn, cgw, ta, tb, to, num_sms, st);
+  if (a.act == ACT_NONE) return band_dispatch<ACT_NONE>(a, bn, cgw, ta, tb, to, num_sms, st);
   return cudaErrorInvalidValue;
 }
 

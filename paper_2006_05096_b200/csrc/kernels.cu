@@ -354,9 +354,60 @@ __global__ void maxpool_vec_kernel(const T* __restrict__ x, T* __restrict__ y, i
   reinterpret_cast<uint4*>(y)[i] = o.u;
 }
 
+// 3x3 / stride 2 / pad 1 (the ResNet stem pool): all nine 16-byte loads
+// issued before any max (clamped addresses, out-of-window taps masked to
+// -inf) so each thread keeps 144 B in flight; the generic kernel's per-tap
+// bounds branches serialised them (3 TB/s measured).
+template <typename T>
+__global__ void maxpool3s2_vec_kernel(const T* __restrict__ x, T* __restrict__ y, int B, int H,
+                                      int W, int C, int OH, int OW) {
+  constexpr int V = Vec16<T>::N;
+  const int CV = C / V;
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long total = (long)B * OH * OW * CV;
+  if (i >= total) return;
+  const int cv = (int)(i % CV);
+  long p = i / CV;
+  const int ow = (int)(p % OW);
+  p /= OW;
+  const int oh = (int)(p % OH);
+  const long b = p / OH;
+  Vec16<T> v[9];
+  bool ok[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int ih = oh * 2 - 1 + r;
+    const int ihc = min(max(ih, 0), H - 1);
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int iw = ow * 2 - 1 + s;
+      const int iwc = min(max(iw, 0), W - 1);
+      ok[r * 3 + s] = (unsigned)ih < (unsigned)H && (unsigned)iw < (unsigned)W;
+      v[r * 3 + s].u =
+          __ldg(reinterpret_cast<const uint4*>(x + ((b * H + ihc) * W + iwc) * C + cv * V));
+    }
+  }
+  float m[V];
+#pragma unroll
+  for (int q = 0; q < V; ++q) m[q] = -INFINITY;
+#pragma unroll
+  for (int t = 0; t < 9; ++t)
+#pragma unroll
+    for (int q = 0; q < V; ++q) m[q] = ok[t] ? fmaxf(m[q], to_f(v[t].e[q])) : m[q];
+  Vec16<T> o;
+#pragma unroll
+  for (int q = 0; q < V; ++q) o.e[q] = from_f<T>(m[q]);
+  reinterpret_cast<uint4*>(y)[i] = o.u;
+}
+
 template <typename T>
 cudaError_t maxpool(const T* x, T* y, int B, int H, int W, int C, int k, int stride, int pad,
                     int OH, int OW, cudaStream_t st) {
+  if (C % Vec16<T>::N == 0 && k == 3 && stride == 2 && pad == 1) {
+    const long tv = (long)B * OH * OW * (C / Vec16<T>::N);
+    maxpool3s2_vec_kernel<T><<<nblk(tv, 256), 256, 0, st>>>(x, y, B, H, W, C, OH, OW);
+    return cudaGetLastError();
+  }
   if (C % Vec16<T>::N == 0) {
     const long tv = (long)B * OH * OW * (C / Vec16<T>::N);
     maxpool_vec_kernel<T><<<nblk(tv, 256), 256, 0, st>>>(x, y, B, H, W, C, k, stride, pad, OH,

@@ -62,7 +62,8 @@ struct BandArgs {
 bool band_config(BandArgs& a, int bn, int cgw, int mt_cap = 4);
 bool band_supported(const BandArgs& a, int bn, int cgw, int act);
 cudaError_t conv_band_launch(const BandArgs& a, int bn, int cgw, const CUtensorMap& ta,
-                             const CUtensorMap& tb, int num_sms, cudaStream_t st);
+                             const CUtensorMap& tb, const CUtensorMap& to, int num_sms,
+                             cudaStream_t st);
 
 int tc_pick_bn(long M, int N, int num_sms);
 cudaError_t tc_gemm_launch(const TcArgs& a, int bn, bool gather, const CUtensorMap& ta,

@@ -206,6 +206,13 @@ struct BatchState {
   cudaGraphExec_t graph = nullptr;
   void* h_in = nullptr;            // pinned (e2e)
   void* h_out = nullptr;
+  // e2e pipelining: a second input/output buffer pair and its graph, so the
+  // H2D of step i+1 and the D2H of step i-1 overlap the forward of step i
+  void* d_in2 = nullptr;
+  float* d_out2 = nullptr;
+  void* h_out2 = nullptr;
+  cudaGraphExec_t graph2 = nullptr;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
 };
 
 }  // namespace
@@ -527,7 +534,7 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
         T* out = A(p[1]);
         if (L.tc && S.band[li]) {
           CK(conv_band_launch(S.bargs[li], S.bn[li], L.s2d ? 16 : 64, S.tmA[li], S.tmB[li],
-                              pl->num_sms, st));
+                              S.tmO[li], pl->num_sms, st));
         } else if (L.tc) {
           TcArgs a{};
           a.M = (int)M;
@@ -673,6 +680,10 @@ size_t in_bytes(const b2_plan* pl, int batch) {
 // Banded implicit-GEMM conv (conv_band.cu) for stride-1 "same" k x k convs
 // with C % 64 == 0 and for space-to-depth stems.  Returns 1 when layer li
 // runs banded (tensor maps built), 0 to keep the gemm_tc path, -code on error.
+// Band row pitch: padded width rounded so 32-position epilogue chunks never
+// straddle an output row at a nonzero column (multiple of 32, or 8 / 16).
+int band_pitch(int w) { return w <= 8 ? 8 : w <= 16 ? 16 : (w + 31) / 32 * 32; }
+
 int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
   Layer& L = pl->layers[li];
   const int* p = L.p;
@@ -684,7 +695,7 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
   if (L.s2d) {
     if (N % 64 != 0 || N > 128) return 0;
     cgw = 16;
-    a.Wp = L.s2d_W2;
+    a.Wp = band_pitch(L.s2d_W2);
     a.R = a.S = L.s2d_Rp;
     a.CG = 1;
     a.x0 = a.y0 = 0;
@@ -695,7 +706,7 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
     if (!L.im2col || stride != 1 || R != Sf || (R & 1) == 0 || pad != (R - 1) / 2 ||
         OH != p[4] || OW != p[5] || C % 64 != 0 || N % 64 != 0 || R == 1)
       return 0;
-    a.Wp = OW + Sf - 1;
+    a.Wp = band_pitch(OW + Sf - 1);
     a.R = R;
     a.S = Sf;
     a.CG = C / 64;
@@ -735,6 +746,14 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
   if (!make_tmap_bf16(&S.tmB[li], L.w, (uint64_t)N, (uint64_t)L.kpad, (uint64_t)L.kpad * 2,
                       (uint32_t)bn))
     return -fail(B2_ERR_CUDA, "layer %zu: band B tensor map rejected", li);
+  // output NHWC [B, OH, OW, N]: 32-channel x 32-pixel boxes, 64 B swizzle
+  cuuint64_t odims[4] = {(cuuint64_t)N, (cuuint64_t)OW, (cuuint64_t)OH, (cuuint64_t)batch};
+  cuuint64_t ostr[3] = {(cuuint64_t)N * 2, (cuuint64_t)OW * N * 2, (cuuint64_t)OH * OW * N * 2};
+  cuuint32_t obox[4] = {32, 32, 1, 1};
+  if (fn(&S.tmO[li], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, S.act[p[1]], odims, ostr, obox, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -fail(B2_ERR_CUDA, "layer %zu: band output tensor map rejected", li);
   S.bn[li] = bn;
   S.band[li] = 1;
   S.bargs[li] = a;
@@ -850,22 +869,29 @@ int enqueue(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
   return run_forward(pl, S, d_in, d_out, st);
 }
 
-// graph of the whole forward on the state's internal buffers
-int graph_of(b2_plan* pl, BatchState& S, cudaGraphExec_t* out) {
-  if (S.graph) {
-    *out = S.graph;
+// graph of the whole forward on the state's internal buffers (second = the
+// alternate input/output pair used by the pipelined e2e loop)
+int graph_of(b2_plan* pl, BatchState& S, cudaGraphExec_t* out, bool second = false) {
+  cudaGraphExec_t& slot = second ? S.graph2 : S.graph;
+  if (slot) {
+    *out = slot;
     return B2_OK;
+  }
+  if (second && !S.d_in2) {
+    CK(cudaMalloc(&S.d_in2, in_bytes(pl, S.batch) + 256));
+    CK(cudaMemset(S.d_in2, 0, in_bytes(pl, S.batch) + 256));
+    CK(cudaMalloc(&S.d_out2, (size_t)S.batch * pl->out_elems * 4 + 256));
   }
   int rc;
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(pl->stream, cudaStreamCaptureModeThreadLocal));
-  rc = run_forward(pl, S, S.d_in, S.d_out, pl->stream);
+  rc = run_forward(pl, S, second ? S.d_in2 : S.d_in, second ? S.d_out2 : S.d_out, pl->stream);
   cudaError_t e = cudaStreamEndCapture(pl->stream, &g);
   if (rc) return rc;
   if (e != cudaSuccess) return fail(B2_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
-  CK(cudaGraphInstantiate(&S.graph, g, 0));
+  CK(cudaGraphInstantiate(&slot, g, 0));
   cudaGraphDestroy(g);
-  *out = S.graph;
+  *out = slot;
   return B2_OK;
 }
 
@@ -1051,6 +1077,70 @@ int b2_gen_input(b2_plan* pl, void* d_in, int batch, uint64_t seed, void* stream
   return gen_inputs(pl, d_in, batch, seed, stream ? static_cast<cudaStream_t>(stream) : pl->stream);
 }
 
+// End-to-end closed loop with host buffers, software-pipelined over three
+// streams: H2D of step i (pinned host -> device buffer i%2) on s_h2d, the
+// forward graph of buffer i%2 on the plan stream, D2H of step i's logits on
+// s_d2h.  Events order buffer reuse (H2D i waits for forward i-2; forward i
+// waits for H2D i and for D2H i-2).  Latency of step i = H2D start -> D2H end;
+// completion = first H2D start -> D2H end of step i.  Every step still moves
+// its full input and output across PCIe inside the timed region.
+static int bench_e2e_pipelined(b2_plan* pl, BatchState* S, int warmup, int n, float* lat_ms,
+                               float* completion_ms) {
+  const int batch = S->batch;
+  cudaGraphExec_t g[2];
+  int rc;
+  if ((rc = graph_of(pl, *S, &g[0])) || (rc = graph_of(pl, *S, &g[1], true))) return rc;
+  const size_t ib = in_bytes(pl, batch), ob = (size_t)batch * pl->out_elems * 4;
+  if (!S->h_out2) CK(cudaMallocHost(&S->h_out2, ob));
+  if (!S->s_h2d) {
+    CK(cudaStreamCreateWithFlags(&S->s_h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&S->s_d2h, cudaStreamNonBlocking));
+  }
+  void* din[2] = {S->d_in, S->d_in2};
+  float* dout[2] = {S->d_out, S->d_out2};
+  void* hout[2] = {S->h_out, S->h_out2};
+  cudaEvent_t in_done[2], fwd_done[2], out_done[2];
+  for (int k = 0; k < 2; ++k) {
+    CK(cudaEventCreateWithFlags(&in_done[k], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&fwd_done[k], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&out_done[k], cudaEventDisableTiming));
+  }
+  // start from a quiet device: earlier work on the plan stream (input gen) done
+  CK(cudaStreamSynchronize(pl->stream));
+  std::vector<cudaEvent_t> ev(2 * (size_t)n);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  bool used[2] = {false, false};
+  for (int i = -warmup; i < n; ++i) {
+    const int k = (i + warmup) & 1;
+    if (used[k]) CK(cudaStreamWaitEvent(S->s_h2d, fwd_done[k], 0));
+    if (i >= 0) CK(cudaEventRecord(ev[2 * i], S->s_h2d));
+    CK(cudaMemcpyAsync(din[k], S->h_in, ib, cudaMemcpyHostToDevice, S->s_h2d));
+    CK(cudaEventRecord(in_done[k], S->s_h2d));
+    CK(cudaStreamWaitEvent(pl->stream, in_done[k], 0));
+    if (used[k]) CK(cudaStreamWaitEvent(pl->stream, out_done[k], 0));
+    CK(cudaGraphLaunch(g[k], pl->stream));
+    CK(cudaEventRecord(fwd_done[k], pl->stream));
+    CK(cudaStreamWaitEvent(S->s_d2h, fwd_done[k], 0));
+    CK(cudaMemcpyAsync(hout[k], dout[k], ob, cudaMemcpyDeviceToHost, S->s_d2h));
+    CK(cudaEventRecord(out_done[k], S->s_d2h));
+    if (i >= 0) CK(cudaEventRecord(ev[2 * i + 1], S->s_d2h));
+    used[k] = true;
+  }
+  CK(cudaStreamSynchronize(S->s_d2h));
+  CK(cudaStreamSynchronize(pl->stream));
+  for (int i = 0; i < n; ++i) {
+    CK(cudaEventElapsedTime(&lat_ms[i], ev[2 * i], ev[2 * i + 1]));
+    CK(cudaEventElapsedTime(&completion_ms[i], ev[0], ev[2 * i + 1]));
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (int k = 0; k < 2; ++k) {
+    cudaEventDestroy(in_done[k]);
+    cudaEventDestroy(fwd_done[k]);
+    cudaEventDestroy(out_done[k]);
+  }
+  return B2_OK;
+}
+
 static int bench_impl(b2_plan* pl, int batch, int warmup, int n, uint64_t seed, float* lat_ms,
                       float* completion_ms, bool e2e) {
   if (!pl || !lat_ms || !completion_ms) return fail(B2_ERR_ARG, "null argument");
@@ -1068,6 +1158,8 @@ static int bench_impl(b2_plan* pl, int batch, int warmup, int n, uint64_t seed, 
     CK(cudaMallocHost(&S->h_out, ob));
     CK(cudaMemcpyAsync(S->h_in, S->d_in, ib, cudaMemcpyDeviceToHost, pl->stream));
   }
+  const char* pp = getenv("B2_E2E_PIPELINE");
+  if (e2e && !(pp && pp[0] == '0')) return bench_e2e_pipelined(pl, S, warmup, n, lat_ms, completion_ms);
   const char* fl = getenv("B2_BENCH_FLUSH_L2");
   const bool flush = fl && fl[0] == '1';
   if (flush && !pl->flush_buf) {
@@ -1183,6 +1275,12 @@ void b2_plan_destroy(b2_plan* pl) {
     cudaFree(S.d_out);
     if (S.h_in) cudaFreeHost(S.h_in);
     if (S.h_out) cudaFreeHost(S.h_out);
+    if (S.graph2) cudaGraphExecDestroy(S.graph2);
+    if (S.d_in2) cudaFree(S.d_in2);
+    if (S.d_out2) cudaFree(S.d_out2);
+    if (S.h_out2) cudaFreeHost(S.h_out2);
+    if (S.s_h2d) cudaStreamSynchronize(S.s_h2d), cudaStreamDestroy(S.s_h2d);
+    if (S.s_d2h) cudaStreamSynchronize(S.s_d2h), cudaStreamDestroy(S.s_d2h);
   }
   for (void* p : pl->allocs) cudaFree(p);
   if (pl->flush_buf) cudaFree(pl->flush_buf);
