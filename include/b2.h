@@ -50,6 +50,8 @@ extern "C" {
 #define B2_ERR_CUDA 3        /* CUDA runtime/launch failure    -> LaunchFailure/CellFailure */
 #define B2_ERR_ARG 4         /* bad argument (batch < 1, NULL) -> InvalidRequest     */
 #define B2_ERR_NODEVICE 5    /* no CUDA device visible         -> LaunchFailure      */
+#define B2_ERR_FUSED 6       /* b2_read_tensor: intermediate fused into its consumer,
+                                never materialised (verification hook only)        */
 
 /* execution dtypes */
 #define B2_DT_FROM_PLAN -1

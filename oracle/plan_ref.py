@@ -310,6 +310,7 @@ def layerwise_errors(plan, read_tensor, x, emulate_bf16: bool):
         W = [w.astype(np.float64) for w in plan.weights]
     out = np.zeros((B, plan.out_elems))
     res = []
+    oracle_t = {}   # oracle values of tensors the executor fused away (never materialised)
     for i, o in enumerate(plan.ops):
         ins, dst = op_io(o)
         if dst is None:
@@ -317,12 +318,18 @@ def layerwise_errors(plan, read_tensor, x, emulate_bf16: bool):
         T = _Bf16Store() if emulate_bf16 else {}
         for t in ins:
             v = read_tensor(t)
+            if v is None:          # fused intermediate: teacher-force from the oracle chain
+                v = oracle_t[t]
             if plan.tensors[t].kind == P.T_IDS:
                 dict.__setitem__(T, t, np.asarray(v, dtype=np.int64).reshape(B, -1))
             else:
                 dict.__setitem__(T, t, np.asarray(v, dtype=np.float64))
         run_op(plan, o, T, W, B, x, out, np.float64)
         ref = np.asarray(T[dst], dtype=np.float64).reshape(B, -1)
-        got = np.asarray(read_tensor(dst), dtype=np.float64).reshape(B, -1)
+        got = read_tensor(dst)
+        if got is None:
+            oracle_t[dst] = ref
+            continue
+        got = np.asarray(got, dtype=np.float64).reshape(B, -1)
         res.append((i, o.name, normwise_err(got, ref)))
     return res

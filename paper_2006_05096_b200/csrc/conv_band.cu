@@ -492,4 +492,269 @@ cudaError_t conv_band_launch(const BandArgs& a, int bn, int cgw, const CUtensorM
   return cudaErrorInvalidValue;
 }
 
+// ============================================================================
+// Stem convolution fused with its 3x3 / stride-2 / pad-1 max-pool.
+//
+// The space-to-depth stem (CGW = 16, 4 x 4 taps, Wp = 128: one conv output
+// row per M tile) is computed two conv rows at a time — the rows 2ph, 2ph+1
+// of pooled row ph — and never written to HBM.  The epilogue drops ReLU'd
+// bf16 conv rows into a 3-slot shared-memory ring (slot = conv row mod 3,
+// columns -1 and OW zero), then all epilogue threads max-pool pooled row ph
+// from ring rows 2ph-1, 2ph, 2ph+1 and store it.  Zero stands in for the
+// pool's -inf padding: every window holds at least one real, post-ReLU (>= 0)
+// value, so the max is unchanged (requires ACT = ReLU; checked on the host).
+//
+// Each CTA owns a contiguous range of pooled rows so conv row 2ph-1 is still
+// in the ring from the previous unit; only the first unit of a range that
+// starts mid-image recomputes it (a third M tile).  Saves the 411 MB conv
+// output write + re-read of the unfused stem/max-pool pair at ResNet b=256.
+constexpr int SP_RING_SLOTS = 3;
+
+B2_DEV void named_bar_epi() { asm volatile("bar.sync 1, %0;" ::"n"(CB_EPI_WARPS * 32) : "memory"); }
+
+__global__ void __launch_bounds__(CB_THREADS, 1)
+    stem_pool_kernel(const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB, const BandArgs a) {
+  constexpr int BN = 64, CGW = 16, R = 4, S = 4, TAPS = 16, RB = 32, B_BLOCK = BN * 128;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int ring_slot = (a.W + 2) * 128;          // (OW + 2) columns x 64 ch x bf16
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + a.a_stages * a.a_stage_bytes;
+  uint8_t* ring = sB + a.kblocks * B_BLOCK;
+  uint64_t* afull = reinterpret_cast<uint64_t*>(ring + SP_RING_SLOTS * ring_slot);
+  uint64_t* aempty = afull + a.a_stages;
+  uint64_t* tfull = aempty + a.a_stages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bres = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
+
+  const int warp = warp_index_uniform();
+  const int lane = threadIdx.x & 31;
+  const int pairs = a.B * a.PH;                   // units: pooled rows of the whole batch
+  const int u0 = (int)((long)blockIdx.x * pairs / gridDim.x);
+  const int u1 = (int)((long)(blockIdx.x + 1) * pairs / gridDim.x);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.a_stages; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], CB_EPI_WARPS);
+    }
+    mbar_init(bres, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, a.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = uniform_u32(*tmem_slot);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      mbar_arrive_expect_tx(bres, (uint32_t)(a.kblocks * B_BLOCK));
+      for (int kb = 0; kb < a.kblocks; ++kb) tma_load_2d(sB + kb * B_BLOCK, &tmB, bres, kb * 64, 0);
+      int as = 0;
+      uint32_t aph = 0;
+      for (int u = u0; u < u1; ++u) {
+        const int img = u / a.PH, ph = u - img * a.PH;
+        const bool halo = u == u0 && ph > 0;
+        mbar_wait(&aempty[as], aph ^ 1);
+        mbar_arrive_expect_tx(&afull[as], (uint32_t)a.a_box_bytes);
+        tma_load_4d(sA + as * a.a_stage_bytes, &tmA, &afull[as], 0, 0, 2 * ph - (halo ? 1 : 0), img);
+        if (++as == a.a_stages) {
+          as = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = make_idesc(128, BN, 1u);
+    uint32_t toff[TAPS];
+#pragma unroll
+    for (int t = 0; t < TAPS; ++t) toff[t] = (uint32_t)(((t / S) * a.Wp + (t % S)) * RB) >> 4;
+    const uint32_t mt_step = (uint32_t)(a.Wp * RB) >> 4;   // one conv row = one s2d row
+    mbar_wait(bres, 0);
+    tc_fence_after();
+    const uint64_t bdesc0 = smem_desc_sw128(smem_u32(sB));
+    int as = 0;
+    uint32_t aph = 0;
+    int it = 0;
+    for (int u = u0; u < u1; ++u, ++it) {
+      const int ph = u % a.PH;
+      const int nt = (u == u0 && ph > 0) ? 3 : 2;
+      const int ab = it & 1;
+      mbar_wait(&tempty[ab], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t dbase = tmem_base + ab * 3 * BN;
+      mbar_wait(&afull[as], aph);
+      tc_fence_after();
+      const uint64_t adesc0 = smem_desc_sw32(smem_u32(sA + as * a.a_stage_bytes));
+      for (int mt = 0; mt < nt; ++mt) {
+#pragma unroll
+        for (int t = 0; t < TAPS; ++t) {
+          const int kg = t * CGW;
+          const uint32_t boff = (uint32_t)((kg >> 6) * B_BLOCK + ((kg >> 4) & 3) * 32) >> 4;
+          if (elect_one())
+            umma_bf16(dbase + mt * BN, adesc0 + mt * mt_step + toff[t], bdesc0 + boff, idesc,
+                      t != 0 ? 1u : 0u);
+        }
+      }
+      if (elect_one()) umma_commit(&aempty[as]);
+      if (++as == a.a_stages) {
+        as = 0;
+        aph ^= 1;
+      }
+      if (elect_one()) umma_commit(&tfull[ab]);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue + pool
+    const int et = threadIdx.x - 64;                 // 0..255
+    const int q = warp & 3;
+    const int eh = (warp - 2) >> 2;
+    for (int i = et; i < SP_RING_SLOTS * ring_slot / 16; i += CB_EPI_WARPS * 32)
+      reinterpret_cast<uint4*>(ring)[i] = make_uint4(0, 0, 0, 0);
+    float bv[32];
+    {
+      const float4* bp = reinterpret_cast<const float4*>(a.bias + eh * 32);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 b4 = __ldg(bp + j);
+        bv[4 * j] = b4.x;
+        bv[4 * j + 1] = b4.y;
+        bv[4 * j + 2] = b4.z;
+        bv[4 * j + 3] = b4.w;
+      }
+    }
+    named_bar_epi();
+    const int ow = q * 32 + lane;                    // this thread's conv column
+    const int cidx = ow + 1;                         // ring column (0 and W+1 stay zero)
+    int it = 0;
+    for (int u = u0; u < u1; ++u, ++it) {
+      const int img = u / a.PH, ph = u - img * a.PH;
+      const bool halo = u == u0 && ph > 0;
+      const int first = 2 * ph - (halo ? 1 : 0);
+      const int nt = halo ? 3 : 2;
+      const int ab = it & 1;
+      mbar_wait(&tfull[ab], (it >> 1) & 1);
+      tc_fence_after();
+      for (int mt = 0; mt < nt; ++mt) {
+        const int cr = first + mt;
+        uint32_t rr[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + ab * 3 * BN + mt * BN + eh * 32, rr);
+        tmem_wait_ld();
+        if (ow < a.W) {
+          uint8_t* col = ring + (cr % SP_RING_SLOTS) * ring_slot + cidx * 128;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 w;
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = fmaxf(__uint_as_float(rr[8 * j + e]) + bv[8 * j + e], 0.f);
+            w.x = pack_bf16x2(v[0], v[1]);
+            w.y = pack_bf16x2(v[2], v[3]);
+            w.z = pack_bf16x2(v[4], v[5]);
+            w.w = pack_bf16x2(v[6], v[7]);
+            const int chunk = eh * 4 + j;
+            *reinterpret_cast<uint4*>(col + ((chunk ^ (cidx & 7)) << 4)) = w;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[ab]);       // accumulators free for unit it + 2
+      if (ph == 0) {                                 // conv row -1 (pool padding): zeros
+        uint8_t* slot = ring + ((SP_RING_SLOTS - 1) % SP_RING_SLOTS) * ring_slot;
+        for (int i = et; i < ring_slot / 16; i += CB_EPI_WARPS * 32)
+          reinterpret_cast<uint4*>(slot)[i] = make_uint4(0, 0, 0, 0);
+      }
+      named_bar_epi();
+      // pooled row ph: max over conv rows 2ph-1..2ph+1, columns 2pw-1..2pw+1
+      const uint8_t* r0 = ring + ((2 * ph + 2) % SP_RING_SLOTS) * ring_slot;
+      const uint8_t* r1 = ring + ((2 * ph) % SP_RING_SLOTS) * ring_slot;
+      const uint8_t* r2 = ring + ((2 * ph + 1) % SP_RING_SLOTS) * ring_slot;
+      bf16* orow = a.pout + ((size_t)(img * a.PH + ph) * a.PW) * BN;
+      for (int i = et; i < a.PW * 8; i += CB_EPI_WARPS * 32) {
+        const int pw = i >> 3, v = i & 7;
+        __nv_bfloat162 m[4];
+        bool init = false;
+#pragma unroll
+        for (int dc = 0; dc < 3; ++dc) {
+          const int c = 2 * pw + dc;                 // ring column of conv col 2pw-1+dc
+          const int off = c * 128 + ((v ^ (c & 7)) << 4);
+#pragma unroll
+          for (int rr_ = 0; rr_ < 3; ++rr_) {
+            const uint8_t* rp = rr_ == 0 ? r0 : rr_ == 1 ? r1 : r2;
+            const uint4 x = *reinterpret_cast<const uint4*>(rp + off);
+            const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&x);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) m[k] = init ? __hmax2(m[k], xh[k]) : xh[k];
+            init = true;
+          }
+        }
+        *reinterpret_cast<uint4*>(orow + pw * BN + v * 8) = *reinterpret_cast<const uint4*>(m);
+      }
+      named_bar_epi();                               // ring reads done before the next unit
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, a.tmem_cols);
+  }
+}
+
+static int stem_pool_smem(const BandArgs& a) {
+  return 1024 + a.a_stages * a.a_stage_bytes + a.kblocks * 64 * 128 +
+         SP_RING_SLOTS * (a.W + 2) * 128 + 8 * (2 * a.a_stages + 5) + 16;
+}
+
+// Geometry for the fused stem: box of 3 conv rows' worth of s2d rows (the
+// halo unit), 3 M tiles per unit at most, resident weights.
+bool stem_pool_config(BandArgs& a) {
+  if (a.R != 4 || a.S != 4 || a.CG != 1 || a.N != 64 || a.Wp != 128 || a.W > 128 ||
+      a.tiles_n != 1 || (a.H & 1) || (a.W & 1) || a.kblocks != 4)
+    return false;
+  a.MT = 3;
+  a.bh = 2;
+  const int box_rows = (3 + a.R - 1) * a.Wp;
+  const int need_rows = 3 * 128 + (a.R - 1) * a.Wp + (a.S - 1);
+  const int rows = ((box_rows > need_rows ? box_rows : need_rows) + 7) / 8 * 8;
+  a.a_box_bytes = box_rows * 32;
+  a.a_stage_bytes = (rows * 32 + 1023) / 1024 * 1024;
+  a.tmem_cols = 512;
+  a.b_resident = 1;
+  a.b_stages = 0;
+  for (a.a_stages = 4; a.a_stages >= 2; --a.a_stages)
+    if (stem_pool_smem(a) <= CB_SMEM_MAX) return true;
+  return false;
+}
+
+cudaError_t stem_pool_launch(const BandArgs& a, const CUtensorMap& ta, const CUtensorMap& tb,
+                             int num_sms, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(stem_pool_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CB_SMEM_MAX);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int pairs = a.B * a.PH;
+  const int grid = pairs < num_sms ? pairs : num_sms;
+  stem_pool_kernel<<<grid, CB_THREADS, stem_pool_smem(a), st>>>(ta, tb, a);
+  return cudaGetLastError();
+}
+
 }  // namespace b2

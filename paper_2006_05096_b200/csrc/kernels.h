@@ -58,9 +58,15 @@ struct BandArgs {
   const float* bias;
   bf16* out;
   int act;
+  // fused 3x3/s2/p1 max-pool epilogue (stem_pool_kernel): pooled output
+  bf16* pout;
+  int PH, PW;
 };
 bool band_config(BandArgs& a, int bn, int cgw, int mt_cap = 4);
 bool band_supported(const BandArgs& a, int bn, int cgw, int act);
+bool stem_pool_config(BandArgs& a);
+cudaError_t stem_pool_launch(const BandArgs& a, const CUtensorMap& ta, const CUtensorMap& tb,
+                             int num_sms, cudaStream_t st);
 cudaError_t conv_band_launch(const BandArgs& a, int bn, int cgw, const CUtensorMap& ta,
                              const CUtensorMap& tb, const CUtensorMap& to, int num_sms,
                              cudaStream_t st);

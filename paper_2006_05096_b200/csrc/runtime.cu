@@ -185,6 +185,8 @@ struct Layer {
   bool s2d = false;
   int s2d_shift = 0, s2d_H2 = 0, s2d_W2 = 0, s2d_Rp = 0, s2d_creal = 0;
   int im2col_mode = 0;      // TcArgs::a_im2col
+  int pool_op = -1;         // s2d stem: index of the 3x3/s2 max-pool fused into its epilogue
+  bool fused = false;       // max-pool executed inside its producer (no launch)
   int gmode = 0;            // see TcArgs::gmode
   int K = 0, kpad = 0, ldw = 0;
 };
@@ -227,6 +229,7 @@ struct b2_plan {
   double flops = 0, weight_bytes = 0;
   std::vector<TensorRec> tensors;
   std::vector<Layer> layers;
+  std::vector<char> virt;    // per tensor: fused away (never materialised)
   std::vector<void*> allocs;
   std::map<int, BatchState> states;
   cudaStream_t stream = nullptr;
@@ -241,6 +244,7 @@ struct b2_plan {
   bool im2col8 = false;      // B2_IM2COL8=1 -> 8-channel-tap im2col TMA for C == 8 stems
                              // (correct, but issue-bound on 2 KB boxes: slower than gather)
   bool use_band = true;      // B2_BAND=0 -> stride-1 k x k convs and s2d stems on gemm_tc
+  bool use_pool_fusion = true;   // B2_POOL_FUSION=0 -> stem and max-pool as two kernels
   int band_max_n = 128;      // B2_BAND_MAX_N: widest conv (output channels) sent to conv_band
   void* identity = nullptr;  // bf16 I[256][256]
   float* zero_bias = nullptr;  // fp32 zeros[8192]: bias of bias-free layers in fused epilogues
@@ -318,6 +322,43 @@ void plan_s2d(b2_plan* pl) {
       L->s2d_W2 = p[13] + 3;
       L->s2d_creal = Li.p[1];
     }
+  }
+}
+
+// Fuse the 3x3 / stride-2 / pad-1 max-pool that is the only consumer of a
+// ReLU space-to-depth stem into the stem's epilogue (conv_band.cu,
+// stem_pool_kernel).  The stem's own output tensor is then never written.
+void plan_fuse_pool(b2_plan* pl) {
+  pl->virt.assign(pl->tensors.size(), 0);
+  if (!pl->use_band || !pl->use_pool_fusion) return;
+  for (size_t ci = 0; ci < pl->layers.size(); ++ci) {
+    Layer& Lc = pl->layers[ci];
+    if (Lc.kind != OP_CONV || !Lc.s2d || Lc.p[14] != ACT_RELU || Lc.p[7] != 64) continue;
+    const int t = Lc.p[1];
+    int pool = -1, users = 0;
+    for (size_t j = 0; j < pl->layers.size(); ++j) {
+      const Layer& Lj = pl->layers[j];
+      if (j == ci) continue;
+      bool uses = false;
+      if (Lj.kind == OP_OUTPUT) {
+        for (int q = 0; q < Lj.p[0]; ++q) uses |= Lj.p[1 + 2 * q] == t;
+      } else if (Lj.kind != OP_INPUT && Lj.kind != OP_TOKENS) {
+        uses = Lj.p[0] == t || (Lj.kind == OP_CONV && Lj.p[15] == t) ||
+               (Lj.kind == OP_LINEAR && Lj.p[8] == t) || (Lj.kind == OP_LAYERNORM && Lj.p[7] == t);
+      }
+      if (uses) {
+        ++users;
+        if (Lj.kind == OP_MAXPOOL && Lj.p[0] == t) pool = (int)j;
+      }
+    }
+    if (users != 1 || pool < 0) continue;
+    const int* q = pl->layers[pool].p;   // in, out, H, W, C, k, stride, pad, OH, OW
+    if (q[5] != 3 || q[6] != 2 || q[7] != 1 || q[2] != Lc.p[12] || q[3] != Lc.p[13] ||
+        q[8] * 2 != q[2] || q[9] * 2 != q[3])
+      continue;
+    Lc.pool_op = pool;
+    pl->layers[pool].fused = true;
+    pl->virt[t] = 1;
   }
 }
 
@@ -532,7 +573,9 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
         const int res_t = conv ? p[15] : p[8];
         const int act = conv ? p[14] : p[7];
         T* out = A(p[1]);
-        if (L.tc && S.band[li]) {
+        if (L.tc && S.band[li] && L.pool_op >= 0) {
+          CK(stem_pool_launch(S.bargs[li], S.tmA[li], S.tmB[li], pl->num_sms, st));
+        } else if (L.tc && S.band[li]) {
           CK(conv_band_launch(S.bargs[li], S.bn[li], L.s2d ? 16 : 64, S.tmA[li], S.tmB[li],
                               S.tmO[li], pl->num_sms, st));
         } else if (L.tc) {
@@ -618,6 +661,7 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
         ++launches;
         break;
       case OP_MAXPOOL:
+        if (L.fused) break;   // computed by the producing stem's epilogue
         CK(maxpool<T>(A(p[0]), A(p[1]), B, p[2], p[3], p[4], p[5], p[6], p[7], p[8], p[9], st));
         ++launches;
         break;
@@ -723,8 +767,17 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
   a.out = reinterpret_cast<bf16*>(S.act[p[1]]);
   a.act = p[14];
   a.bias = L.bias ? L.bias : pl->zero_bias;
-  if (!band_config(a, bn, cgw) || !band_supported(a, bn, cgw, a.act)) return 0;
-  if ((long)a.B * a.nbands * a.tiles_n < pl->num_sms) {   // small batch: more, smaller units
+  if (L.pool_op >= 0) {
+    const int* q = pl->layers[L.pool_op].p;
+    a.pout = reinterpret_cast<bf16*>(S.act[q[1]]);
+    a.PH = q[8];
+    a.PW = q[9];
+    if (!stem_pool_config(a))
+      return -fail(B2_ERR_UNSUPPORTED, "layer %zu: fused stem/max-pool geometry rejected", li);
+  } else if (!band_config(a, bn, cgw) || !band_supported(a, bn, cgw, a.act)) {
+    return 0;
+  }
+  if (L.pool_op < 0 && (long)a.B * a.nbands * a.tiles_n < pl->num_sms) {   // small batch: more, smaller units
     BandArgs t = a;
     if (band_config(t, bn, cgw, 1) && band_supported(t, bn, cgw, t.act)) a = t;
   }
@@ -736,7 +789,8 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
   cuuint64_t dims[4] = {(cuuint64_t)cin, (cuuint64_t)win, (cuuint64_t)hin, (cuuint64_t)batch};
   cuuint64_t str[3] = {(cuuint64_t)cin * 2, (cuuint64_t)win * cin * 2,
                        (cuuint64_t)hin * win * cin * 2};
-  cuuint32_t box[4] = {(cuuint32_t)cgw, (cuuint32_t)a.Wp, (cuuint32_t)(a.bh + a.R - 1), 1};
+  const int box_h = L.pool_op >= 0 ? 3 + a.R - 1 : a.bh + a.R - 1;
+  cuuint32_t box[4] = {(cuuint32_t)cgw, (cuuint32_t)a.Wp, (cuuint32_t)box_h, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   if (fn(&S.tmA[li], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, S.act[p[0]], dims, str, box, es,
          CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -959,6 +1013,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* i8 = getenv("B2_IM2COL8")) pl->im2col8 = i8[0] == '1';
   if (const char* sd = getenv("B2_S2D")) pl->use_s2d = sd[0] != '0';
   if (const char* bd = getenv("B2_BAND")) pl->use_band = bd[0] != '0';
+  if (const char* pf = getenv("B2_POOL_FUSION")) pl->use_pool_fusion = pf[0] != '0';
   if (const char* bm = getenv("B2_BAND_MAX_N")) pl->band_max_n = atoi(bm);
   cudaGetDevice(&pl->device);
   cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, pl->device);
@@ -991,6 +1046,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   }
   int rc = validate_ops(pl);
   if (!rc) plan_s2d(pl);
+  if (!rc) plan_fuse_pool(pl);
   if (!rc) rc = upload_weights(pl, d + pos, wr, len - 4 - pos);
   if (!rc && pl->dtype == B2_DT_BF16) {
     std::vector<float> eye(256 * 256, 0.f);
@@ -1035,7 +1091,7 @@ int b2_plan_info(const b2_plan* pl, double* flops, double* wbytes, int* launches
   if (wbytes) *wbytes = pl->weight_bytes;
   if (launches) {
     int n = 0;
-    for (const Layer& L : pl->layers) n += L.kind == OP_OUTPUT ? L.p[0] : 1;
+    for (const Layer& L : pl->layers) n += L.kind == OP_OUTPUT ? L.p[0] : L.fused ? 0 : 1;
     *launches = n;
   }
   if (dtype) *dtype = pl->dtype;
@@ -1238,6 +1294,8 @@ int b2_read_tensor(b2_plan* pl, int batch, int tensor, void* host_out, size_t by
   if (it == pl->states.end()) return fail(B2_ERR_ARG, "no forward has run at batch %d", batch);
   const size_t need = (size_t)batch * pl->tensors[tensor].elems * elem_size(pl, tensor);
   if (bytes < need) return fail(B2_ERR_ARG, "buffer too small (%zu < %zu)", bytes, need);
+  if (pl->virt[tensor])
+    return fail(B2_ERR_FUSED, "tensor %d is fused into its consumer (not materialised)", tensor);
   int rc = check_device(pl);
   if (rc) return rc;
   CK(cudaStreamSynchronize(pl->stream));

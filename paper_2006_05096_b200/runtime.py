@@ -21,7 +21,7 @@ from .plan import DT_BF16, DT_FP32, IN_TOKENS
 
 LIB_PATH = Path(__file__).resolve().parent / "libb2.so"
 
-B2_OK, B2_ERR_FORMAT, B2_ERR_UNSUPPORTED, B2_ERR_CUDA, B2_ERR_ARG, B2_ERR_NODEVICE = range(6)
+B2_OK, B2_ERR_FORMAT, B2_ERR_UNSUPPORTED, B2_ERR_CUDA, B2_ERR_ARG, B2_ERR_NODEVICE, B2_ERR_FUSED = range(7)
 DT_FROM_PLAN = -1
 
 _lib = None
@@ -172,7 +172,9 @@ class Plan:
 
     def read_tensor(self, batch: int, tensor: int, elems: int, kind: int) -> np.ndarray:
         """Activation `tensor` of the last forward at `batch`, as float64 (or
-        int32 ids) — the verification hook used by the layerwise parity tests."""
+        int32 ids) — the verification hook used by the layerwise parity tests.
+        None when the executor fused the tensor into its consumer (never
+        materialised, e.g. the stem output under the fused stem/max-pool)."""
         if kind == 1:
             buf = np.empty(batch * elems, dtype=np.int32)
         elif self.dtype == DT_BF16:
@@ -180,6 +182,8 @@ class Plan:
         else:
             buf = np.empty(batch * elems, dtype=np.float32)
         rc = self._lib.b2_read_tensor(self._h, batch, tensor, buf.ctypes.data, buf.nbytes)
+        if rc == B2_ERR_FUSED:
+            return None
         if rc != B2_OK:
             _raise(rc, "read_tensor")
         if buf.dtype == np.uint16:

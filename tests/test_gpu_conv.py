@@ -85,3 +85,45 @@ def test_stem_s2d(gpu_required, batch):
 def test_other_convs(gpu_required, k, stride, H, C, N):
     """Strided / 5x5 convs: band path for stride 1 k x k, im2col GEMM otherwise."""
     check(conv_plan(H, H, C, N, k, stride), 4)
+
+
+def stem_pool_plan(seed=0):
+    """ResNet stem: 7x7/2 conv (3 -> 64, ReLU) then 3x3/2 max-pool."""
+    b = P.PlanBuilder("stem_pool")
+    x = b.tensor(224, 224, 8)
+    b.in_elems = 3 * 224 * 224
+    b.op_p(P.OP_INPUT, [x, 3, 224, 224, 8])
+    rng = np.random.default_rng(seed)
+    y = b.tensor(112, 112, 64)
+    w = rng.standard_normal((64, 7, 7, 8)) * (1.0 / np.sqrt(147))
+    w[..., 3:] = 0.0
+    b.op_p(P.OP_CONV, [x, y, b.weight(w), b.weight(rng.standard_normal(64) * 0.1), 224, 224, 8,
+                       64, 7, 7, 2, 3, 112, 112, 1, -1])
+    z = b.tensor(56, 56, 64)
+    b.op_p(P.OP_MAXPOOL, [y, z, 112, 112, 64, 3, 2, 1, 56, 56])
+    b.out_elems = b.tensors[z].elems
+    b.op_p(P.OP_OUTPUT, [1, z, 0])
+    return b.build(P.DT_FP32)
+
+
+@pytest.mark.parametrize("batch", [1, 3, 16])
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_stem_maxpool(gpu_required, monkeypatch, batch, fused):
+    """Stem + max-pool: fused (stem_pool_kernel; the stem output is never
+    materialised, so the pool is checked against the oracle's own stem) and
+    unfused.  Batch 3 and 16 put unit ranges across image boundaries and start
+    ranges mid-image (the recomputed halo row)."""
+    monkeypatch.setenv("B2_POOL_FUSION", fused)
+    blob = stem_pool_plan()
+    pl = P.decode(blob)
+    x = plan_ref.make_inputs(pl, batch, 5)
+    plan = R.Plan(blob, P.DT_BF16)
+    try:
+        out = plan.predict(x)
+        assert np.isfinite(out).all()
+        rt = lambda t: plan.read_tensor(batch, t, pl.tensors[t].elems, pl.tensors[t].kind)
+        assert (rt(pl.ops[1][1]) is None) == (fused == "1")
+        errs = plan_ref.layerwise_errors(pl, rt, x, True)
+        assert errs and all(e[2] <= TOL for e in errs), errs
+    finally:
+        plan.close()
