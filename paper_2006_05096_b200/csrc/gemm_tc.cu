@@ -64,10 +64,13 @@ B2_DEV void add_bf16x8(float* v, const uint4& u) {
 
 // TMA-store epilogue of one warp, specialised on the activation so the
 // per-element math is branch-free.
+// Tiles t = t0, t0 + tstep, ... < ntiles; tile t covers rows
+// (t / tiles_n) * mstride + mofs.  `tempty_remote` != 0: signal accumulator
+// release on the CTA-pair leader's barrier (cluster address) instead of ours.
 template <int BN, int ACT>
 B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint64_t* tfull,
                     uint64_t* tempty, uint32_t tmem_base, int ntiles, int lg, int ew, int eh,
-                    int lane) {
+                    int lane, int t0, int tstep, int mstride, int mofs, uint32_t tempty_remote) {
   const bool has_res = a.res != nullptr;
   int it = 0;
   // 32-column chunks split between the two warps of each TMEM lane
@@ -77,10 +80,10 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint
   uint8_t* obuf = sEpi + ew * 4096;
   uint32_t oi = 0;
   const uint32_t swz = (lane >> 1) & 3;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+  for (int t = t0; t < ntiles; t += tstep, ++it) {
     const int as = it & 1;
     const uint32_t aph = (it >> 1) & 1;
-    const int m0 = (t / a.tiles_n) * TC_BM;
+    const int m0 = (t / a.tiles_n) * mstride + mofs;
     const int n0 = (t % a.tiles_n) * BN;
     const int row0 = m0 + lg * 32;
     const int row = row0 + lane;
@@ -165,7 +168,10 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint
     }
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&tempty[as]);
+    if (lane == 0) {
+      if (tempty_remote) mbar_arrive_cluster(tempty_remote + as * 8);
+      else mbar_arrive(&tempty[as]);
+    }
   }
   if (lane == 0) bulk_wait<0>();
 }
@@ -353,11 +359,11 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
       }
     } else if (BN >= 32 && a.tma_epi) {
       switch (a.act) {
-        case ACT_RELU: epi_tma<BN, ACT_RELU>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane); break;
-        case ACT_RELU6: epi_tma<BN, ACT_RELU6>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane); break;
-        case ACT_GELU: epi_tma<BN, ACT_GELU>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane); break;
-        case ACT_TANH: epi_tma<BN, ACT_TANH>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane); break;
-        default: epi_tma<BN, ACT_NONE>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane); break;
+        case ACT_RELU: epi_tma<BN, ACT_RELU>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, blockIdx.x, gridDim.x, TC_BM, 0, 0u); break;
+        case ACT_RELU6: epi_tma<BN, ACT_RELU6>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, blockIdx.x, gridDim.x, TC_BM, 0, 0u); break;
+        case ACT_GELU: epi_tma<BN, ACT_GELU>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, blockIdx.x, gridDim.x, TC_BM, 0, 0u); break;
+        case ACT_TANH: epi_tma<BN, ACT_TANH>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, blockIdx.x, gridDim.x, TC_BM, 0, 0u); break;
+        default: epi_tma<BN, ACT_NONE>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, blockIdx.x, gridDim.x, TC_BM, 0, 0u); break;
       }
     } else {
       // direct path (narrow tiles / N not a multiple of 8): 16-byte stores
@@ -523,6 +529,191 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
   }
 }
 
+// ============================================================================
+// CTA-pair GEMM (cta_group::2): a cluster of two CTAs on one TPC computes a
+// 256 x BN tile with M = 256 UMMAs issued by the leader.  Each CTA loads its
+// own 128 A rows and HALF of the BN weight rows; the MMA reads the other half
+// from the peer's shared memory.  Per SM this halves the weight traffic and
+// the weight smem per stage (A 16 KB + B BN/2 x 128 B), so the ring is ~1.5x
+// deeper for the same MMA work — the late-ResNet / BERT GEMMs are bound by
+// operand delivery, not by the tensor pipe (ncu: MMA thread waiting on TMA
+// ~45% with 128 x 256 single-CTA tiles).
+//
+// Barriers: full[s] lives in the leader (both CTAs' TMA loads complete_tx on
+// it, the leader alone expects 2 x stage bytes); empty[s] and tfull[] exist in
+// both CTAs and receive the leader's multicast commits; the leader's
+// tempty[] collects the epilogue warps of both CTAs (16 arrivals).
+template <int BN>
+struct Tc2Cfg {
+  static constexpr int A_BYTES = TC_BM * TC_BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * TC_BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_RAW = (TC_SMEM_MAX - TC_EPI_BYTES - 1024 - TC_BAR_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 10 ? 10 : STAGES_RAW;
+  static constexpr int THREADS = (2 + TC_EPI_WARPS) * 32;
+  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + TC_EPI_BYTES + 1024 + TC_BAR_BYTES;
+};
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<BN>::THREADS, 1)
+    tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA,
+                    const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmO,
+                    const __grid_constant__ CUtensorMap tmR,
+                    const __grid_constant__ CUtensorMap tmI, const TcArgs a) {
+  using Cfg = Tc2Cfg<BN>;
+  constexpr int ST = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + ST * Cfg::A_BYTES;
+  uint8_t* sEpi = sB + ST * Cfg::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + TC_EPI_BYTES);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = warp_index_uniform();
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int ntiles = a.tiles_m * a.tiles_n;
+  const int KT = a.kblocks + a.res_kblocks;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * TC_EPI_WARPS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    if (a.res_kblocks) {
+      tma_prefetch_desc(&tmR);
+      tma_prefetch_desc(&tmI);
+    }
+    tma_prefetch_desc(&tmO);
+  }
+  cluster_sync();                       // barrier inits visible to the peer
+  if (warp == 1) tmem_alloc_pair(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = uniform_u32(*tmem_slot);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      const int cpb = a.C >> 6;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < ntiles; t += ncl) {
+        const int m0 = (t / a.tiles_n) * (2 * TC_BM) + (int)rank * TC_BM;
+        const int n0 = (t % a.tiles_n) * BN;
+        const int nb = n0 + (int)rank * (BN / 2);          // this CTA's half of the weights
+        int iw0 = 0, ih0 = 0, img = 0;
+        if (a.a_im2col) {
+          img = m0 / a.OHW;
+          const int rem = m0 - img * a.OHW;
+          const int oh = rem / a.OW;
+          ih0 = oh * a.stride - a.pad;
+          iw0 = (rem - oh * a.OW) * a.stride - a.pad;
+        }
+        for (int kb = 0; kb < KT; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t fl = mapa_shared(&full[stage], 0);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+          uint8_t* dA = sA + stage * Cfg::A_BYTES;
+          uint8_t* dB = sB + stage * Cfg::B_BYTES;
+          if (kb >= a.kblocks) {
+            const int j = kb - a.kblocks;
+            tma_load_2d_pair(dA, &tmR, fl, n0 + j * TC_BK, m0);
+            tma_load_2d_pair(dB, &tmI, fl, j * TC_BK, (int)rank * (BN / 2));
+          } else {
+            if (a.a_im2col) {
+              const int tap = kb / cpb;
+              const int c0 = (kb - tap * cpb) << 6;
+              const int r = tap / a.S;
+              const int s2 = tap - r * a.S;
+              tma_load_im2col_4d_pair(dA, &tmA, fl, c0, iw0, ih0, img, (uint16_t)s2, (uint16_t)r);
+            } else {
+              tma_load_2d_pair(dA, &tmA, fl, kb * TC_BK, m0);
+            }
+            tma_load_2d_pair(dB, &tmB, fl, kb * TC_BK, nb);
+          }
+          if (++stage == ST) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader, whole warp)
+    if (rank == 0) {
+      constexpr uint32_t idesc = make_idesc(2 * TC_BM, BN, 1u);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cid; t < ntiles; t += ncl, ++it) {
+        const int as = it & 1;
+        mbar_wait(&tempty[as], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dt = tmem_base + as * BN;
+        for (int kb = 0; kb < KT; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = smem_desc_sw128(smem_u32(sA + stage * Cfg::A_BYTES));
+          const uint64_t bd = smem_desc_sw128(smem_u32(sB + stage * Cfg::B_BYTES));
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k)
+            if (elect_one()) umma_bf16_pair(dt, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          if (elect_one()) umma_commit_pair(&empty[stage]);
+          if (++stage == ST) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (elect_one()) umma_commit_pair(&tfull[as]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int lg = warp & 3;
+    const int ew = warp - 2;
+    const int eh = ew >> 2;
+    const uint32_t trem = rank == 0 ? 0u : mapa_shared(&tempty[0], 0);
+    switch (a.act) {
+#define B2_EPI2(ACTV)                                                                            \
+  epi_tma<BN, ACTV>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, cid, ncl, \
+                    2 * TC_BM, (int)rank * TC_BM, trem)
+      case ACT_RELU: B2_EPI2(ACT_RELU); break;
+      case ACT_RELU6: B2_EPI2(ACT_RELU6); break;
+      case ACT_GELU: B2_EPI2(ACT_GELU); break;
+      case ACT_TANH: B2_EPI2(ACT_TANH); break;
+      default: B2_EPI2(ACT_NONE); break;
+#undef B2_EPI2
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();                       // the peer is done with our barriers and TMEM
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 
 template <int BN, bool G>
@@ -543,6 +734,52 @@ static cudaError_t launch_bn(TcArgs a, const CUtensorMap& ta, const CUtensorMap&
   const int grid = tiles < num_sms ? tiles : num_sms;
   kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(ta, tb, to, tr, ti, a);
   return cudaGetLastError();
+}
+
+template <int BN>
+static cudaError_t launch_pair(TcArgs a, const CUtensorMap& ta, const CUtensorMap& tb,
+                               const CUtensorMap& to, const CUtensorMap& tr, const CUtensorMap& ti,
+                               int num_sms, cudaStream_t st) {
+  using Cfg = Tc2Cfg<BN>;
+  auto kern = tc_gemm2_kernel<BN>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int tiles = a.tiles_m * a.tiles_n;
+  const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
+  kern<<<2 * pairs, Cfg::THREADS, Cfg::SMEM, st>>>(ta, tb, to, tr, ti, a);
+  return cudaGetLastError();
+}
+
+// CTA-pair launch: a.tiles_m counts 256-row pair tiles; tb / ti boxes are BN/2 rows.
+cudaError_t tc_gemm2_launch(const TcArgs& a, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
+                            const CUtensorMap& to, const CUtensorMap& tr, const CUtensorMap& ti,
+                            int num_sms, cudaStream_t st) {
+  if (bn == 256) return launch_pair<256>(a, ta, tb, to, tr, ti, num_sms, st);
+  if (bn == 128) return launch_pair<128>(a, ta, tb, to, tr, ti, num_sms, st);
+  return cudaErrorInvalidValue;
+}
+
+// BN for the CTA-pair kernel: fewest pair-tile waves, MMA time per tile ~ BN.
+int tc2_pick_bn(long M, int N, int num_sms) {
+  const long tm = (M + 2 * TC_BM - 1) / (2 * TC_BM);
+  const int pairs = num_sms / 2;
+  long best_cost = -1;
+  int best = 0;
+  for (int bn : {256, 128}) {
+    if (bn / 2 >= N) continue;
+    const long tiles = tm * ((N + bn - 1) / bn);
+    const long cost = (tiles + pairs - 1) / pairs * bn;
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = bn;
+    }
+  }
+  return best;
 }
 
 int tc_pick_bn(long M, int N, int num_sms) {

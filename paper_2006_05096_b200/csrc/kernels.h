@@ -72,6 +72,10 @@ cudaError_t conv_band_launch(const BandArgs& a, int bn, int cgw, const CUtensorM
                              cudaStream_t st);
 
 int tc_pick_bn(long M, int N, int num_sms);
+int tc2_pick_bn(long M, int N, int num_sms);
+cudaError_t tc_gemm2_launch(const TcArgs& a, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
+                            const CUtensorMap& to, const CUtensorMap& tr, const CUtensorMap& ti,
+                            int num_sms, cudaStream_t st);
 cudaError_t tc_gemm_launch(const TcArgs& a, int bn, bool gather, const CUtensorMap& ta,
                            const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& tr,
                            const CUtensorMap& ti, int num_sms, cudaStream_t st);

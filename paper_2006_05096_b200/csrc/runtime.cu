@@ -204,6 +204,7 @@ struct BatchState {
   std::vector<char> fold;          // per layer: residual folded into the MMA
   std::vector<CUtensorMap> tmI;    // per layer: identity [256 x 256] (box rows = BN) for the fold
   std::vector<char> band;          // per layer: banded implicit-GEMM conv (conv_band.cu)
+  std::vector<char> pair;          // per layer: CTA-pair GEMM (tc_gemm2_kernel)
   std::vector<BandArgs> bargs;     // per layer (band): geometry chosen by band_config
   cudaGraphExec_t graph = nullptr;
   void* h_in = nullptr;            // pinned (e2e)
@@ -244,6 +245,8 @@ struct b2_plan {
   bool im2col8 = false;      // B2_IM2COL8=1 -> 8-channel-tap im2col TMA for C == 8 stems
                              // (correct, but issue-bound on 2 KB boxes: slower than gather)
   bool use_band = true;      // B2_BAND=0 -> stride-1 k x k convs and s2d stems on gemm_tc
+  bool use_pair = true;      // B2_PAIR=0 -> single-CTA tc_gemm only
+  long pair_min_m = 4096;    // B2_PAIR_MIN_M: smallest M sent to the CTA-pair GEMM
   bool use_pool_fusion = true;   // B2_POOL_FUSION=0 -> stem and max-pool as two kernels
   int band_max_n = 128;      // B2_BAND_MAX_N: widest conv (output channels) sent to conv_band
   void* identity = nullptr;  // bf16 I[256][256]
@@ -622,9 +625,16 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
           a.epi_debug = pl->epi_mode == 2 ? 0 : pl->epi_mode;
           a.stages = pl->stages_override;
           a.res_kblocks = S.fold[li] ? bn / 64 : 0;
-          CK(tc_gemm_launch(a, bn, L.gather, L.gather ? S.tmB[li] : S.tmA[li], S.tmB[li],
-                            S.tmO[li], S.fold[li] ? S.tmR[li] : S.tmO[li],
-                            S.fold[li] ? S.tmI[li] : S.tmO[li], pl->num_sms, st));
+          if (S.pair[li]) {
+            a.tiles_m = (int)((M + 255) / 256);
+            CK(tc_gemm2_launch(a, bn, S.tmA[li], S.tmB[li], S.tmO[li],
+                               S.fold[li] ? S.tmR[li] : S.tmO[li],
+                               S.fold[li] ? S.tmI[li] : S.tmO[li], pl->num_sms, st));
+          } else {
+            CK(tc_gemm_launch(a, bn, L.gather, L.gather ? S.tmB[li] : S.tmA[li], S.tmB[li],
+                              S.tmO[li], S.fold[li] ? S.tmR[li] : S.tmO[li],
+                              S.fold[li] ? S.tmI[li] : S.tmO[li], pl->num_sms, st));
+          }
         } else {
           GemmSimtArgs a{};
           a.M = (int)M;
@@ -842,6 +852,7 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
   S.fold.assign(pl->layers.size(), 0);
   S.tmI.resize(pl->layers.size());
   S.band.assign(pl->layers.size(), 0);
+  S.pair.assign(pl->layers.size(), 0);
   S.bargs.resize(pl->layers.size());
   for (size_t li = 0; li < pl->layers.size(); ++li) {
     Layer& L = pl->layers[li];
@@ -859,10 +870,20 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     const bool conv = L.kind == OP_CONV;
     const int N = conv ? p[7] : p[5];
     const long M = conv ? (long)batch * p[12] * p[13] : (long)batch * p[6];
-    const int bn = tc_pick_bn(M, N, pl->num_sms);
+    // CTA-pair (cta_group::2) GEMM for the TMA-fed shapes big enough to fill
+    // the pairs; weight boxes then hold BN/2 rows (each CTA loads half)
+    // measured (tools/gemm_sweep.sh): pairs win on long-K, wide-N GEMMs
+    // (K >= 1024, BN = 256: +7% at 16384x4096x4096, +7% at 50176x1024x256)
+    // and lose on short-K / residual-fold / BN = 128 shapes
+    const bool pair_ok = pl->use_pair && !L.s2d && !L.gather && (!L.im2col || L.im2col_mode == 1) &&
+                         N % 8 == 0 && M >= pl->pair_min_m && L.K >= 1024 &&
+                         tc2_pick_bn(M, N, pl->num_sms) == 256;
+    const int bn = pair_ok ? tc2_pick_bn(M, N, pl->num_sms) : tc_pick_bn(M, N, pl->num_sms);
     S.bn[li] = bn;
+    S.pair[li] = pair_ok;
+    const uint32_t bbox = pair_ok ? bn / 2 : bn;
     if (!make_tmap_bf16(&S.tmB[li], L.w, (uint64_t)N, (uint64_t)L.kpad, (uint64_t)L.kpad * 2,
-                        (uint32_t)bn))
+                        bbox))
       return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeTiled(B) failed", li);
     if (L.s2d) {
       // A: overlapping 4D view of the space-to-depth input — element (k, ow, Y, n)
@@ -898,7 +919,7 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     if (res_t >= 0 && bn >= 64 && N % 8 == 0 && L.K <= pl->fold_max_k && pl->identity) {
       if (!make_tmap_bf16(&S.tmR[li], S.act[res_t], (uint64_t)M, (uint64_t)N, (uint64_t)N * 2,
                           128) ||
-          !make_tmap_bf16(&S.tmI[li], pl->identity, 256, 256, 512, (uint32_t)bn))
+          !make_tmap_bf16(&S.tmI[li], pl->identity, 256, 256, 512, bbox))
         return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeTiled(res/identity) failed", li);
       S.fold[li] = 1;
     }
@@ -1013,6 +1034,8 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* i8 = getenv("B2_IM2COL8")) pl->im2col8 = i8[0] == '1';
   if (const char* sd = getenv("B2_S2D")) pl->use_s2d = sd[0] != '0';
   if (const char* bd = getenv("B2_BAND")) pl->use_band = bd[0] != '0';
+  if (const char* pr = getenv("B2_PAIR")) pl->use_pair = pr[0] != '0';
+  if (const char* pm = getenv("B2_PAIR_MIN_M")) pl->pair_min_m = atol(pm);
   if (const char* pf = getenv("B2_POOL_FUSION")) pl->use_pool_fusion = pf[0] != '0';
   if (const char* bm = getenv("B2_BAND_MAX_N")) pl->band_max_n = atoi(bm);
   cudaGetDevice(&pl->device);

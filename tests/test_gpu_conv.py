@@ -127,3 +127,47 @@ def test_stem_maxpool(gpu_required, monkeypatch, batch, fused):
         assert errs and all(e[2] <= TOL for e in errs), errs
     finally:
         plan.close()
+
+
+def linear_plan(K, N, res, seed=0):
+    """One LINEAR (+ optional residual from a second LINEAR), ReLU."""
+    b = P.PlanBuilder("lin")
+    x = b.tensor(K)
+    b.in_elems = K
+    b.op_p(P.OP_INPUT, [x, K, 1, 1, K])
+    rng = np.random.default_rng(seed)
+    r = -1
+    if res:
+        r = b.tensor(N)
+        b.op_p(P.OP_LINEAR, [x, r, b.weight(rng.standard_normal((N, K)) / np.sqrt(K)),
+                             b.weight(rng.standard_normal(N) * 0.1), K, N, 1, 0, -1, K])
+    y = b.tensor(N)
+    b.op_p(P.OP_LINEAR, [x, y, b.weight(rng.standard_normal((N, K)) / np.sqrt(K)),
+                         b.weight(rng.standard_normal(N) * 0.1), K, N, 1, 1, r, K])
+    b.out_elems = b.tensors[y].elems
+    b.op_p(P.OP_OUTPUT, [1, y, 0])
+    return b.build(P.DT_FP32)
+
+
+@pytest.mark.parametrize("M,K,N,res", [
+    (4173, 256, 1024, True),    # CTA-pair GEMM, residual fold, ragged M (pair tail)
+    (8192, 1024, 256, False),
+    (6000, 512, 192, False),    # N not a multiple of the tile: BN = 128, ragged N
+    (50176, 64, 256, True),
+])
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_gemm_shapes(gpu_required, monkeypatch, M, K, N, res, pair):
+    """Row-parallel GEMMs through the CTA-pair (cta_group::2) kernel and the
+    single-CTA kernel; M is the batch of a one-row-per-sample plan."""
+    monkeypatch.setenv("B2_PAIR", pair)
+    check(linear_plan(K, N, res), M)
+
+
+@pytest.mark.parametrize("H,C,N,k,stride,batch", [
+    (7, 512, 512, 3, 1, 128),    # layer4 3x3 via im2col, CTA pair
+    (14, 256, 256, 3, 1, 40),    # layer3 3x3
+    (14, 512, 512, 3, 2, 96),    # strided 3x3 (im2col, pair)
+    (14, 1024, 2048, 1, 2, 96),  # strided 1x1 downsample
+])
+def test_late_convs(gpu_required, H, C, N, k, stride, batch):
+    check(conv_plan(H, H, C, N, k, stride), batch)
