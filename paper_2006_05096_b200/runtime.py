@@ -69,7 +69,8 @@ def load_library(path: os.PathLike | None = None):
     global _lib
     with _lib_lock:
         if _lib is None:
-            p = Path(path) if path else LIB_PATH
+            # B2_LIB: alternate build of the same ABI (A/B timing tools only)
+            p = Path(path) if path else Path(os.environ.get("B2_LIB", LIB_PATH))
             if not p.exists():
                 raise errors.LaunchFailure(
                     f"libb2.so not built at {p}; run `python -m paper_2006_05096_b200.build`")
