@@ -59,6 +59,8 @@ __global__ void __launch_bounds__(128, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = uniform_u32(*tslot);
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (warp == 0) {   // converged warp, elected lane issues (common.cuh)
     if (elect_one()) {
@@ -167,8 +169,7 @@ cudaError_t attention_tc(const CUtensorMap& tm_qkv, bf16* out, int B, int H, cud
     if (e != cudaSuccess) return e;
     cfg = true;
   }
-  attn_tc_kernel<<<B * H, 128, AT_SMEM, st>>>(tm_qkv, out, H);
-  return cudaGetLastError();
+  return launch_pdl(attn_tc_kernel, dim3(B * H), dim3(128), AT_SMEM, st, tm_qkv, out, H);
 }
 
 }  // namespace b2

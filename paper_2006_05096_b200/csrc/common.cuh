@@ -177,6 +177,33 @@ template <int N> B2_DEV void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// tcgen05 kernels are launched with programmatic stream serialisation: the
+// next kernel's CTAs are scheduled (barrier init, TMEM alloc, tensor-map
+// prefetch) while this one drains, and block in pdl_wait() until it has
+// completed and its writes are visible.  Both are no-ops without the launch
+// attribute.
+B2_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+B2_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();   // runtime switch (B2_PDL, default on)
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+}
+
 // ---------------------------------------------------------------- warp-uniform helpers
 // ptxas keeps TMEM addresses and UMMA descriptors in uniform registers only
 // when it can prove them warp-uniform; values derived from threadIdx or from

@@ -119,6 +119,8 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = uniform_u32(*tmem_slot);
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -449,8 +451,7 @@ static cudaError_t band_launch_t(const BandArgs& a, const CUtensorMap& ta, const
   }
   const int units = a.B * a.nbands * a.tiles_n;
   const int grid = units < num_sms ? units : num_sms;
-  kern<<<grid, CB_THREADS, band_smem_bytes(a, BN), st>>>(ta, tb, to, a);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(CB_THREADS), band_smem_bytes(a, BN), st, ta, tb, to, a);
 }
 
 template <int ACT>
@@ -557,6 +558,8 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = uniform_u32(*tmem_slot);
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -753,8 +756,8 @@ cudaError_t stem_pool_launch(const BandArgs& a, const CUtensorMap& ta, const CUt
   }
   const int pairs = a.B * a.PH;
   const int grid = pairs < num_sms ? pairs : num_sms;
-  stem_pool_kernel<<<grid, CB_THREADS, stem_pool_smem(a), st>>>(ta, tb, a);
-  return cudaGetLastError();
+  return launch_pdl(stem_pool_kernel, dim3(grid), dim3(CB_THREADS), stem_pool_smem(a), st, ta, tb,
+                    a);
 }
 
 }  // namespace b2

@@ -97,6 +97,14 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint
                        ? __ldg(reinterpret_cast<const uint4*>(rrow + eh * 32) + q)
                        : make_uint4(0, 0, 0, 0);
     }
+    // bias of the first chunk, fetched before the accumulator wait (a global
+    // load per chunk on the critical path cost ~3 us per exposed tile)
+    float4 bnext[8];
+    {
+      const float4* bp = reinterpret_cast<const float4*>(a.bias + n0 + eh * 32);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) bnext[q] = a.bias ? __ldg(bp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     mbar_wait(&tfull[as], aph);
     tc_fence_after();
     const uint32_t taddr = tmem_base + (uint32_t(lg * 32) << 16) + as * BN;
@@ -117,19 +125,17 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint
         }
       }
       float bv[32];
-      if (a.bias) {
-        const float4* bp = reinterpret_cast<const float4*>(a.bias + n0 + c);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 b4 = __ldg(bp + q);
-          bv[4 * q] = b4.x;
-          bv[4 * q + 1] = b4.y;
-          bv[4 * q + 2] = b4.z;
-          bv[4 * q + 3] = b4.w;
-        }
-      } else {
+      for (int q = 0; q < 8; ++q) {
+        bv[4 * q] = bnext[q].x;
+        bv[4 * q + 1] = bnext[q].y;
+        bv[4 * q + 2] = bnext[q].z;
+        bv[4 * q + 3] = bnext[q].w;
+      }
+      if (c + 64 < BN && a.bias) {
+        const float4* bp = reinterpret_cast<const float4*>(a.bias + n0 + c + 64);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) bv[j] = 0.f;
+        for (int q = 0; q < 8; ++q) bnext[q] = __ldg(bp + q);
       }
       tmem_wait_ld();
       float v[32];
@@ -201,7 +207,16 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
   const int lane = threadIdx.x & 31;
   const int ntiles = a.tiles_m * a.tiles_n;
 
+  __shared__ unsigned long long ts[8];    // B2_GEMM_TS phase timestamps (globaltimer, ns)
+  auto stamp = [&](int i) {
+    if (a.ts_debug) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      ts[i] = g;
+    }
+  };
   if (threadIdx.x == 0) {
+    stamp(0);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], GATHER ? 1 + 128 : 1);
       mbar_init(&empty[s], 1);
@@ -226,6 +241,9 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = uniform_u32(*tmem_slot);
+  pdl_wait();                 // previous kernel's outputs (our A / residual) are complete
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) stamp(1);
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -314,6 +332,7 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
         for (int kb = 0; kb < a.kblocks + a.res_kblocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          if (it == 0 && kb == 0 && lane == 0) stamp(2);
           const bool tap8 = a.a_im2col == 2 && kb < a.kblocks;
           const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
           const uint64_t ad = tap8 ? smem_desc_kmajor_noswizzle(a_addr, 2048, 128)
@@ -331,6 +350,7 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
         }
         if (elect_one()) umma_commit(&tfull[as]);
       }
+      if (lane == 0) stamp(3);
     }
   } else if (warp < 2 + TC_EPI_WARPS) {
     // ------------------------------------------------------------ epilogue
@@ -521,8 +541,16 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
     cp_async_wait<0>();
   }
 
+  if (warp == 2 && lane == 0) stamp(4);
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0 && a.ts_debug) {
+    stamp(5);
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    printf("b2ts %d %u %llu %llu %llu %llu %llu %llu\n", blockIdx.x, smid, ts[0], ts[1], ts[2],
+           ts[3], ts[4], ts[5]);
+  }
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
@@ -609,6 +637,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<BN>::THREADS,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = uniform_u32(*tmem_slot);
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -732,8 +762,7 @@ static cudaError_t launch_bn(TcArgs a, const CUtensorMap& ta, const CUtensorMap&
   if (a.stages <= 0 || a.stages > Cfg::MAX_STAGES) a.stages = Cfg::MAX_STAGES;
   const int tiles = a.tiles_m * a.tiles_n;
   const int grid = tiles < num_sms ? tiles : num_sms;
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(ta, tb, to, tr, ti, a);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, ta, tb, to, tr, ti, a);
 }
 
 template <int BN>
@@ -751,8 +780,8 @@ static cudaError_t launch_pair(TcArgs a, const CUtensorMap& ta, const CUtensorMa
   }
   const int tiles = a.tiles_m * a.tiles_n;
   const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  kern<<<2 * pairs, Cfg::THREADS, Cfg::SMEM, st>>>(ta, tb, to, tr, ti, a);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(2 * pairs), dim3(Cfg::THREADS), Cfg::SMEM, st, ta, tb, to, tr, ti,
+                    a);
 }
 
 // CTA-pair launch: a.tiles_m counts 256-row pair tiles; tb / ti boxes are BN/2 rows.

@@ -32,6 +32,7 @@ struct TcArgs {
   int tma_epi;          // epilogue through smem + TMA store (N % 8 == 0, BN >= 64)
   int stages;           // smem pipeline depth (0 = the most that fits)
   int epi_debug;        // 0 normal; 1 drain TMEM only (no math/stores) — profiling aid
+  int ts_debug;         // B2_GEMM_TS=1: first/last CTA print phase timestamps — profiling aid
   int OH;               // s2d stems: output rows per image (M tile = one output row)
   int out3d;            // output TMA map is [rows, OW, C]: box rows clip at OW
   int a_im2col;         // A via TMA: 3 = space-to-depth stem (one output row per M tile,

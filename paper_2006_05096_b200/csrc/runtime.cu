@@ -17,6 +17,9 @@
 #include "common.cuh"
 #include "kernels.h"
 
+static bool g_pdl = true;   // B2_PDL=0 -> plain stream-ordered launches
+bool pdl_enabled() { return g_pdl; }
+
 namespace {
 
 using namespace b2;
@@ -252,6 +255,7 @@ struct b2_plan {
   void* identity = nullptr;  // bf16 I[256][256]
   float* zero_bias = nullptr;  // fp32 zeros[8192]: bias of bias-free layers in fused epilogues
   int stages_override = 0;   // B2_STAGES
+  int ts_debug = 0;          // B2_GEMM_TS
 };
 
 namespace {
@@ -623,6 +627,7 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
           }
           a.tma_epi = bn >= 32 && N % 8 == 0 && pl->epi_mode != 2;
           a.epi_debug = pl->epi_mode == 2 ? 0 : pl->epi_mode;
+          a.ts_debug = pl->ts_debug;
           a.stages = pl->stages_override;
           a.res_kblocks = S.fold[li] ? bn / 64 : 0;
           if (S.pair[li]) {
@@ -1029,6 +1034,8 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   pl->force_simt = fs && fs[0] == '1';
   if (const char* em = getenv("B2_EPI_MODE")) pl->epi_mode = atoi(em);
   if (const char* sg = getenv("B2_STAGES")) pl->stages_override = atoi(sg);
+  if (const char* gt = getenv("B2_GEMM_TS")) pl->ts_debug = atoi(gt);
+  if (const char* pd = getenv("B2_PDL")) g_pdl = pd[0] != '0';
   if (const char* fk = getenv("B2_FOLD_MAX_K")) pl->fold_max_k = atoi(fk);
   if (const char* ic = getenv("B2_IM2COL")) pl->use_im2col = ic[0] != '0';
   if (const char* i8 = getenv("B2_IM2COL8")) pl->im2col8 = i8[0] == '1';

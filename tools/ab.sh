@@ -1,13 +1,8 @@
-# A/B: baseline build (ab/libb2_base.so, HEAD) vs working tree, same box, interleaved
 cd $GRAFT_REPO_ROOT
-for rep in 1 2; do
-for lib in ab/libb2_base.so paper_2006_05096_b200/libb2.so; do
-  echo "== $lib"
-  export B2_LIB=$PWD/$lib
-  for args in "12544 2048 512" "12544 512 2048 res" "300 2048 512" "50176 1024 256"; do
-    B2_PAIR=0 timeout 60 python tools/gemm_micro.py $args
-  done
-  timeout 60 python tools/conv_micro.py 256 7 7 512 512 3 1
-  timeout 60 python tools/conv_micro.py 4 7 7 512 512 3 1
-done
+for pd in 0 1; do
+  export B2_PDL=$pd
+  echo "== PDL=$pd"
+  timeout 60 python tools/chain_micro.py 18944 256 20
+  timeout 60 python tools/chain_micro.py 256 1024 20
+  timeout 120 python bench.py --no-cpu --steps 30 --warmup 5 | python3 -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench', d['ms_per_step'], d['value'], d['e2e']['value'], {k: v['p50_ms'] for k, v in d['per_batch'].items()})"
 done
