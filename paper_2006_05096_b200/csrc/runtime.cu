@@ -256,6 +256,7 @@ struct b2_plan {
   float* zero_bias = nullptr;  // fp32 zeros[8192]: bias of bias-free layers in fused epilogues
   int stages_override = 0;   // B2_STAGES
   int ts_debug = 0;          // B2_GEMM_TS
+  int force_bn = 0;          // B2_FORCE_BN
 };
 
 namespace {
@@ -883,7 +884,12 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     const bool pair_ok = pl->use_pair && !L.s2d && !L.gather && (!L.im2col || L.im2col_mode == 1) &&
                          N % 8 == 0 && M >= pl->pair_min_m && L.K >= 1024 &&
                          tc2_pick_bn(M, N, pl->num_sms) == 256;
-    const int bn = pair_ok ? tc2_pick_bn(M, N, pl->num_sms) : tc_pick_bn(M, N, pl->num_sms);
+    int bn = pair_ok ? tc2_pick_bn(M, N, pl->num_sms) : tc_pick_bn(M, N, pl->num_sms);
+    // Memory-bound shapes (one K block, or im2col A that each extra N tile
+    // re-gathers) want the widest tile: measured 56x56x64->256 128 -> 115 us,
+    // 56x56x256->28x28x512/s2 110 -> 72 us with BN = 256 instead of 128.
+    if (!pair_ok && N % 256 == 0 && (L.kpad <= 64 || (L.im2col && L.im2col_mode == 1))) bn = 256;
+    if (pl->force_bn && !pair_ok && N % pl->force_bn == 0) bn = pl->force_bn;   // B2_FORCE_BN (tuning aid)
     S.bn[li] = bn;
     S.pair[li] = pair_ok;
     const uint32_t bbox = pair_ok ? bn / 2 : bn;
@@ -1035,6 +1041,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* em = getenv("B2_EPI_MODE")) pl->epi_mode = atoi(em);
   if (const char* sg = getenv("B2_STAGES")) pl->stages_override = atoi(sg);
   if (const char* gt = getenv("B2_GEMM_TS")) pl->ts_debug = atoi(gt);
+  if (const char* fb = getenv("B2_FORCE_BN")) pl->force_bn = atoi(fb);
   if (const char* pd = getenv("B2_PDL")) g_pdl = pd[0] != '0';
   if (const char* fk = getenv("B2_FOLD_MAX_K")) pl->fold_max_k = atoi(fk);
   if (const char* ic = getenv("B2_IM2COL")) pl->use_im2col = ic[0] != '0';

@@ -1,8 +1,8 @@
 cd $GRAFT_REPO_ROOT
-for pd in 0 1; do
-  export B2_PDL=$pd
-  echo "== PDL=$pd"
-  timeout 60 python tools/chain_micro.py 18944 256 20
-  timeout 60 python tools/chain_micro.py 256 1024 20
-  timeout 120 python bench.py --no-cpu --steps 30 --warmup 5 | python3 -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench', d['ms_per_step'], d['value'], d['e2e']['value'], {k: v['p50_ms'] for k, v in d['per_batch'].items()})"
-done
+timeout 60 python tools/conv_micro.py 256 14 14 512 512 3 2
+timeout 60 python tools/conv_micro.py 256 28 28 256 256 3 2
+timeout 60 python tools/conv_micro.py 256 7 7 512 512 3 1
+timeout 60 python tools/conv_micro.py 256 14 14 256 256 3 1
+timeout 60 python tools/conv_micro.py 256 14 14 1024 2048 1 2
+timeout 60 python tools/conv_micro.py 256 28 28 512 1024 1 2
+timeout 120 python bench.py --no-cpu --steps 30 --warmup 5 --no-sweep | python3 -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench', d['ms_per_step'], d['value'], d['e2e']['value'])"
