@@ -1,8 +1,6 @@
 cd $GRAFT_REPO_ROOT
-timeout 60 python tools/conv_micro.py 256 14 14 512 512 3 2
-timeout 60 python tools/conv_micro.py 256 28 28 256 256 3 2
-timeout 60 python tools/conv_micro.py 256 7 7 512 512 3 1
-timeout 60 python tools/conv_micro.py 256 14 14 256 256 3 1
-timeout 60 python tools/conv_micro.py 256 14 14 1024 2048 1 2
-timeout 60 python tools/conv_micro.py 256 28 28 512 1024 1 2
-timeout 120 python bench.py --no-cpu --steps 30 --warmup 5 --no-sweep | python3 -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench', d['ms_per_step'], d['value'], d['e2e']['value'])"
+for fk in 256 512 1024; do
+  export B2_FOLD_MAX_K=$fk
+  timeout 60 python tools/gemm_micro.py 12544 512 2048 res
+  timeout 60 python tools/gemm_micro.py 3136 512 2048 res
+done
