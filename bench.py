@@ -126,7 +126,8 @@ def cpu_baseline(model: str, plan_bytes: bytes, seconds: float = 12.0, batch: in
 
 
 def roofline(plan, plan_bytes: bytes, batch: int, pk: dict) -> dict:
-    """Dominant kernel = the tcgen05 GEMM/implicit-GEMM (every conv/linear op).
+    """Dominant kernels = the tcgen05 GEMM / implicit-GEMM / banded-conv family
+    (every conv/linear op: tc_gemm, tc_gemm2, conv_band, stem_pool).
     achieved = algorithmic FLOPs of those launches / their summed CUDA-event
     durations (per-op events on the plan's stream, eager replay)."""
     from paper_2006_05096_b200 import plan as P
@@ -154,7 +155,8 @@ def roofline(plan, plan_bytes: bytes, batch: int, pk: dict) -> dict:
         traffic = json.loads(tp.read_text()).get("tc_gemm_bytes_per_launch")
     return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
-            "kernel": "b2::tc_gemm_kernel (tcgen05 GEMM / implicit-GEMM conv)",
+            "kernel": "tcgen05 conv/GEMM kernels (tc_gemm, tc_gemm2 CTA-pair, conv_band, "
+                      "stem_pool) over every conv/linear op",
             "launches_per_step": launches, "avg_launch_ms": round(t_gemm / launches, 5),
             "share_of_step": round(t_gemm / t_all, 4),
             "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({pk['_source']})"}
