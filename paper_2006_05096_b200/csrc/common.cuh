@@ -19,11 +19,26 @@ typedef __nv_bfloat16 bf16;
 
 enum { ACT_NONE = 0, ACT_RELU = 1, ACT_RELU6 = 2, ACT_GELU = 3, ACT_TANH = 4 };
 
+// GELU(x) = x/2 (1 + erf(x / sqrt 2)) with erf from Abramowitz & Stegun
+// 7.1.26 (|error| <= 1.5e-7, below fp32 resolution of the result; one
+// MUFU.EX2 + one MUFU.RCP + 6 FMAs): libdevice erff's branches made the GELU
+// epilogue the bottleneck of the BERT FFN GEMM (119 vs 90 us with ReLU).
+B2_DEV float gelu_erf(float v) {
+  const float z = fabsf(v) * 0.70710678118654752f;
+  const float t = __fdividef(1.f, fmaf(0.3275911f, z, 1.f));
+  const float poly =
+      t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f),
+                       -0.284496736f),
+               0.254829592f);
+  const float erfz = 1.f - poly * __expf(-z * z);
+  return 0.5f * v * (1.f + copysignf(erfz, v));
+}
+
 B2_DEV float act_apply(float v, int act) {
   switch (act) {
     case ACT_RELU: return fmaxf(v, 0.f);
     case ACT_RELU6: return fminf(fmaxf(v, 0.f), 6.f);
-    case ACT_GELU: return 0.5f * v * (1.f + erff(v * 0.70710678118654752f));
+    case ACT_GELU: return gelu_erf(v);
     case ACT_TANH: return tanhf(v);
     default: return v;
   }
@@ -32,7 +47,7 @@ B2_DEV float act_apply(float v, int act) {
 template <int ACT> B2_DEV float act_t(float v) {
   if constexpr (ACT == ACT_RELU) return fmaxf(v, 0.f);
   else if constexpr (ACT == ACT_RELU6) return fminf(fmaxf(v, 0.f), 6.f);
-  else if constexpr (ACT == ACT_GELU) return 0.5f * v * (1.f + erff(v * 0.70710678118654752f));
+  else if constexpr (ACT == ACT_GELU) return gelu_erf(v);
   else if constexpr (ACT == ACT_TANH) return tanhf(v);
   else return v;
 }

@@ -250,6 +250,7 @@ struct b2_plan {
   bool use_band = true;      // B2_BAND=0 -> stride-1 k x k convs and s2d stems on gemm_tc
   bool use_pair = true;      // B2_PAIR=0 -> single-CTA tc_gemm only
   long pair_min_m = 4096;    // B2_PAIR_MIN_M: smallest M sent to the CTA-pair GEMM
+  int pair_min_k = 1024;     // B2_PAIR_MIN_K: shortest K sent to the CTA-pair GEMM
   bool use_pool_fusion = true;   // B2_POOL_FUSION=0 -> stem and max-pool as two kernels
   int band_max_n = 128;      // B2_BAND_MAX_N: widest conv (output channels) sent to conv_band
   void* identity = nullptr;  // bf16 I[256][256]
@@ -882,7 +883,7 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     // (K >= 1024, BN = 256: +7% at 16384x4096x4096, +7% at 50176x1024x256)
     // and lose on short-K / residual-fold / BN = 128 shapes
     const bool pair_ok = pl->use_pair && !L.s2d && !L.gather && (!L.im2col || L.im2col_mode == 1) &&
-                         N % 8 == 0 && M >= pl->pair_min_m && L.K >= 1024 &&
+                         N % 8 == 0 && M >= pl->pair_min_m && L.K >= pl->pair_min_k &&
                          tc2_pick_bn(M, N, pl->num_sms) == 256;
     int bn = pair_ok ? tc2_pick_bn(M, N, pl->num_sms) : tc_pick_bn(M, N, pl->num_sms);
     // Memory-bound shapes (one K block, or im2col A that each extra N tile
@@ -1050,6 +1051,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* bd = getenv("B2_BAND")) pl->use_band = bd[0] != '0';
   if (const char* pr = getenv("B2_PAIR")) pl->use_pair = pr[0] != '0';
   if (const char* pm = getenv("B2_PAIR_MIN_M")) pl->pair_min_m = atol(pm);
+  if (const char* pk = getenv("B2_PAIR_MIN_K")) pl->pair_min_k = atoi(pk);
   if (const char* pf = getenv("B2_POOL_FUSION")) pl->use_pool_fusion = pf[0] != '0';
   if (const char* bm = getenv("B2_BAND_MAX_N")) pl->band_max_n = atoi(bm);
   cudaGetDevice(&pl->device);

@@ -1,6 +1,4 @@
 cd $GRAFT_REPO_ROOT
-for fk in 256 512 1024; do
-  export B2_FOLD_MAX_K=$fk
-  timeout 60 python tools/gemm_micro.py 12544 512 2048 res
-  timeout 60 python tools/gemm_micro.py 3136 512 2048 res
-done
+for rep in 1 2; do for lib in ab/libb2_base.so paper_2006_05096_b200/libb2.so; do
+  B2_LIB=$PWD/$lib timeout 120 python tools/profile_ops.py bert 128 > gpurun_out/o.log 2>&1; echo "$lib $(head -1 gpurun_out/o.log)"; grep "N=3072" gpurun_out/o.log | head -2
+done; done
