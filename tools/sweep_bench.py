@@ -1,0 +1,127 @@
+"""C4 profile sweep on this box through the product path (BASELINE configs[3]):
+register -> convert (b200 plugins) -> Profiler.run_sweep with one b200 worker
+per model on each GPU, device-timed cells (n=100, warmup=10), reference CSV.
+
+Writes <out>.csv (the reference profile-table schema) and <out>.json: sweep
+wall time on the GPUs used, per-cell device time, and an LPT projection of
+the same cells onto 2/4/8 GPUs (labelled "projected": measured cell times +
+measured per-worker start, partitioned by sweeprun.lpt_partition).
+
+    python tools/sweep_bench.py profiles/r1_sweep_c4 [--models resnet50,...] [--batches 1,2,...]
+"""
+import argparse
+import json
+import os
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2006_05096_b200 import converter, toyformat, zoo  # noqa: E402
+from paper_2006_05096_b200.dispatcher import Dispatcher, b200_template  # noqa: E402
+from paper_2006_05096_b200.hub import Hub, TensorSpec  # noqa: E402
+from paper_2006_05096_b200.profiler import results_to_csv  # noqa: E402
+from paper_2006_05096_b200.profiler.sweep import JobStore, Profiler  # noqa: E402
+from paper_2006_05096_b200.profiler.types import ProfilingJob, SweepSpec  # noqa: E402
+from paper_2006_05096_b200.sweeprun import lpt_partition  # noqa: E402
+from paper_2006_05096_b200.telemetry import NvmlProvider, Telemetry  # noqa: E402
+
+
+def register(hub: Hub, name: str):
+    if name == "mlp":
+        rec = hub.register("mlp", "toy", toyformat.canonical_json(zoo.make_mlp_graph(0)),
+                           [TensorSpec("x", [-1, 784])])
+        src = "toy"
+    elif name == "bert":
+        rec = hub.register("bert", "transformers-bert",
+                           converter.pack_bert(zoo.make_torch_model("bert", 0)),
+                           [TensorSpec("input_ids", [-1, 128])])
+        src = "transformers-bert"
+    else:
+        rec = hub.register(name, "torchvision",
+                           converter.pack_torchvision(zoo.make_torch_model(name, 0), name),
+                           [TensorSpec("x", [-1, 3, 224, 224])])
+        src = "torchvision"
+    plugin = [p for p in converter.b200_plugins((src,)) if p.target_format == "b200-bf16"][0]
+    return rec, hub.convert(rec, plugin)
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("out")
+    ap.add_argument("--models", default="mlp,mobilenet_v2,resnet50,bert,vgg16")
+    ap.add_argument("--batches", default="1,2,4,8,16,32,64,128,256")
+    ap.add_argument("--requests", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    args = ap.parse_args()
+    models = args.models.split(",")
+    batches = [int(b) for b in args.batches.split(",")]
+    hub = Hub()
+    t0 = time.perf_counter()
+    variants = {m: register(hub, m) for m in models}
+    convert_s = time.perf_counter() - t0
+    tel = Telemetry(NvmlProvider())
+    tel.sample_devices()
+    work = Path(tempfile.mkdtemp(prefix="b2sweep_"))
+    disp = Dispatcher(hub, {"b200": b200_template()}, work, tel.device_ids)
+    tel.instance_pid_resolver = disp.pid_of
+    tel.instance_device_resolver = disp.device_of
+    prof = Profiler(hub, disp, tel, JobStore(hub.store))
+    rows, cells, per_model = [], [], {}
+    t_sweep = time.perf_counter()
+    try:
+        for m in models:
+            rec, var = variants[m]
+            job = ProfilingJob(f"c4-{m}", rec.id, var.id,
+                               SweepSpec(batch_sizes=batches, devices=["gpu:0"], backends=["b200"],
+                                         protocols=["grpc-style"],
+                                         requests_per_cell=args.requests,
+                                         warmup_requests=args.warmup))
+            tm = time.perf_counter()
+            res = prof.run_sweep(job)
+            per_model[m] = {"wall_s": round(time.perf_counter() - tm, 3),
+                            "failed_cells": list(job.failed_cells)}
+            rows += res
+            for r in res:
+                # device time of the cell's timed requests (+ warm-up at the same rate)
+                dev_s = (args.requests + args.warmup) * r.p50_latency_ms / 1e3
+                cells.append({"model": m, "batch": r.batch_size,
+                              "samples_s": round(r.peak_throughput, 1),
+                              "p50_ms": round(r.p50_latency_ms, 4),
+                              "p99_ms": round(r.p99_latency_ms, 4), "device_s": dev_s})
+    finally:
+        disp.shutdown()
+    wall = time.perf_counter() - t_sweep
+    setup = {m: max(0.0, per_model[m]["wall_s"] - sum(c["device_s"] for c in cells
+                                                      if c["model"] == m)) for m in models}
+    proj = {}
+    for k in (1, 2, 4, 8):
+        # each GPU runs its LPT share of cells; a model's worker start is paid on
+        # every GPU that hosts one of its cells
+        bins = lpt_partition(cells, lambda c: c["device_s"], k)
+        loads = [sum(c["device_s"] for c in b) + sum(setup[m] for m in {c["model"] for c in b})
+                 for b in bins]
+        proj[str(k)] = round(max(loads), 3)
+    out = Path(args.out)
+    out.parent.mkdir(parents=True, exist_ok=True)
+    out.with_suffix(".csv").write_text(results_to_csv(rows))
+    summary = {"config": "C4: " + ",".join(models) + " x batches " + args.batches,
+               "requests_per_cell": args.requests, "warmup_requests": args.warmup,
+               "gpus_measured": 1, "sweep_wall_s_measured": round(wall, 3),
+               "convert_s": round(convert_s, 3), "per_model": per_model,
+               "sweep_wall_s_projected_lpt": proj,
+               "projection": "LPT over measured per-cell device time + per-model worker "
+                             "start/graph capture (measured wall - device time), one worker "
+                             "per (model, GPU)",
+               "cells": cells}
+    out.with_suffix(".json").write_text(json.dumps(summary, indent=1))
+    print(json.dumps({k: summary[k] for k in ("sweep_wall_s_measured", "sweep_wall_s_projected_lpt",
+                                               "per_model")}))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
