@@ -75,19 +75,33 @@ static_assert(sizeof(TensorRec) == 24, "tensor rec");
 static_assert(sizeof(WeightRec) == 32, "weight rec");
 static_assert(sizeof(OpRec) == 128, "op rec");
 
+// CRC-32 (IEEE, reflected), slice-by-8: ~8x the byte-table loop, which
+// cost ~0.5 s of plan creation on the 436 MB BERT blob.
 uint32_t crc32(const uint8_t* p, size_t n) {
-  static uint32_t table[256];
+  static uint32_t table[8][256];
   static bool init = false;
   if (!init) {
     for (uint32_t i = 0; i < 256; ++i) {
       uint32_t c = i;
       for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
-      table[i] = c;
+      table[0][i] = c;
     }
+    for (uint32_t i = 0; i < 256; ++i)
+      for (int s = 1; s < 8; ++s) table[s][i] = (table[s - 1][i] >> 8) ^ table[0][table[s - 1][i] & 0xFF];
     init = true;
   }
   uint32_t c = 0xFFFFFFFFu;
-  for (size_t i = 0; i < n; ++i) c = table[(c ^ p[i]) & 0xFF] ^ (c >> 8);
+  size_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    uint32_t lo, hi;
+    memcpy(&lo, p + i, 4);
+    memcpy(&hi, p + i + 4, 4);
+    lo ^= c;
+    c = table[7][lo & 0xFF] ^ table[6][(lo >> 8) & 0xFF] ^ table[5][(lo >> 16) & 0xFF] ^
+        table[4][lo >> 24] ^ table[3][hi & 0xFF] ^ table[2][(hi >> 8) & 0xFF] ^
+        table[1][(hi >> 16) & 0xFF] ^ table[0][hi >> 24];
+  }
+  for (; i < n; ++i) c = table[0][(c ^ p[i]) & 0xFF] ^ (c >> 8);
   return c ^ 0xFFFFFFFFu;
 }
 
@@ -196,7 +210,8 @@ struct Layer {
 
 struct BatchState {
   int batch = 0;
-  std::vector<void*> act;          // per tensor
+  std::vector<void*> act;          // per tensor (slices of arena)
+  void* arena = nullptr;
   void* d_in = nullptr;            // internal input buffer
   float* d_out = nullptr;          // internal output buffer
   std::vector<int> bn;             // per layer (tc)
@@ -254,6 +269,8 @@ struct b2_plan {
   bool use_pool_fusion = true;   // B2_POOL_FUSION=0 -> stem and max-pool as two kernels
   int band_max_n = 128;      // B2_BAND_MAX_N: widest conv (output channels) sent to conv_band
   void* identity = nullptr;  // bf16 I[256][256]
+  void* stage = nullptr;     // weight-upload staging (plan creation only)
+  size_t stage_bytes = 0;
   float* zero_bias = nullptr;  // fp32 zeros[8192]: bias of bias-free layers in fused epilogues
   int stages_override = 0;   // B2_STAGES
   int ts_debug = 0;          // B2_GEMM_TS
@@ -276,17 +293,26 @@ int upload_f32(b2_plan* pl, const float* src, size_t n, float** out) {
   return B2_OK;
 }
 
-// host fp32 -> device T (via an fp32 staging buffer and a conversion kernel)
+// host fp32 -> device T via a plan-lifetime fp32 staging buffer and a
+// conversion kernel on the legacy stream (the next synchronous cudaMemcpy
+// into the staging buffer is ordered after it); freed once all weights are
+// up.  Per-weight cudaMalloc/cudaFree/cudaDeviceSynchronize of the staging
+// buffer cost seconds of worker start-up on BERT / VGG.
 template <typename T> int upload_as(b2_plan* pl, const std::vector<float>& h, void** out) {
-  float* stage = nullptr;
-  CK(cudaMalloc(&stage, h.size() * sizeof(float) + 16));
-  CK(cudaMemcpy(stage, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+  const size_t need = h.size() * sizeof(float) + 16;
+  if (need > pl->stage_bytes) {
+    if (pl->stage) {
+      CK(cudaDeviceSynchronize());
+      CK(cudaFree(pl->stage));
+    }
+    CK(cudaMalloc(&pl->stage, need));
+    pl->stage_bytes = need;
+  }
+  CK(cudaMemcpy(pl->stage, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
   T* d = nullptr;
   CK(cudaMalloc(&d, h.size() * sizeof(T) + 16));
   pl->allocs.push_back(d);
-  CK(convert_f32<T>(stage, d, (long)h.size(), 0));
-  CK(cudaDeviceSynchronize());
-  CK(cudaFree(stage));
+  CK(convert_f32<T>(static_cast<const float*>(pl->stage), d, (long)h.size(), 0));
   pl->weight_bytes += h.size() * sizeof(T);
   *out = d;
   return B2_OK;
@@ -840,14 +866,21 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
   BatchState S;
   S.batch = batch;
   S.act.resize(pl->tensors.size(), nullptr);
+  // one arena per batch size (one cudaMalloc + one memset instead of one per
+  // tensor: ~0.3 s of first-cell set-up at ResNet b=256); 1 KB-aligned slices
+  std::vector<size_t> off(pl->tensors.size());
+  size_t arena = 0;
   for (size_t t = 0; t < pl->tensors.size(); ++t) {
     size_t bytes = (size_t)batch * pl->tensors[t].elems * elem_size(pl, (int)t);
     for (const Layer& L : pl->layers)   // space-to-depth input: [B, H2, W2, 16] bf16
       if (L.kind == OP_INPUT && L.s2d && L.p[0] == (int)t)
         bytes = (size_t)batch * L.s2d_H2 * L.s2d_W2 * 16 * 2;
-    CK(cudaMalloc(&S.act[t], bytes + 256));
-    CK(cudaMemset(S.act[t], 0, bytes + 256));
+    off[t] = arena;
+    arena += (bytes + 256 + 1023) / 1024 * 1024;
   }
+  CK(cudaMalloc(&S.arena, arena));
+  CK(cudaMemset(S.arena, 0, arena));
+  for (size_t t = 0; t < pl->tensors.size(); ++t) S.act[t] = static_cast<uint8_t*>(S.arena) + off[t];
   CK(cudaMalloc(&S.d_in, in_bytes(pl, batch) + 256));
   CK(cudaMemset(S.d_in, 0, in_bytes(pl, batch) + 256));
   CK(cudaMalloc(&S.d_out, (size_t)batch * pl->out_elems * 4 + 256));
@@ -1095,6 +1128,12 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
       std::vector<float> z(8192, 0.f);
       rc = upload_f32(pl, z.data(), z.size(), &pl->zero_bias);
     }
+  }
+  if (pl->stage) {
+    if (cudaDeviceSynchronize() != cudaSuccess && !rc) rc = fail(B2_ERR_CUDA, "weight upload failed");
+    cudaFree(pl->stage);
+    pl->stage = nullptr;
+    pl->stage_bytes = 0;
   }
   if (!rc) {
     // algorithmic FLOPs (2 per MAC) of the contraction ops
@@ -1367,7 +1406,7 @@ void b2_plan_destroy(b2_plan* pl) {
   for (auto& kv : pl->states) {
     BatchState& S = kv.second;
     if (S.graph) cudaGraphExecDestroy(S.graph);
-    for (void* p : S.act) cudaFree(p);
+    cudaFree(S.arena);
     cudaFree(S.d_in);
     cudaFree(S.d_out);
     if (S.h_in) cudaFreeHost(S.h_in);
