@@ -236,7 +236,7 @@ def decode(blob: bytes) -> Plan:
         raise PlanFormatError("bad magic, not a b200-plan")
     if version != VERSION:
         raise PlanFormatError(f"unsupported plan version {version}")
-    if zlib.crc32(blob[:-4]) != struct.unpack("<I", blob[-4:])[0]:
+    if zlib.crc32(memoryview(blob)[:-4]) != struct.unpack("<I", blob[-4:])[0]:
         raise PlanFormatError("CRC mismatch, plan corrupted")
     pos = _HDR.size
     need = pos + nt * _TEN.size + nw * _WGT.size + no * _OP.size + meta_len

@@ -44,20 +44,24 @@ NO_DEVICE_EXIT = 3
 def load_plan_bytes(data: bytes) -> bytes:
     """b200-plan bytes from a variant file (plans pass through; toy graphs are
     lowered with the toy converter, so a reference toy variant also loads)."""
-    if data[:4] == P.MAGIC:
-        P.decode(data)   # validate: magic, CRC, tables
-        return data
-    graph = toyformat.load_model(data)
-    return zoo.emit_toy(graph, "toy").build(P.DT_FP32)
+    return load_plan(data)[0]
+
+
+def load_plan(data: bytes) -> tuple[bytes, dict]:
+    """(plan bytes, plan meta) — decoded once (magic, CRC, tables)."""
+    if data[:4] != P.MAGIC:
+        graph = toyformat.load_model(data)
+        data = zoo.emit_toy(graph, "toy").build(P.DT_FP32)
+    return data, P.decode(data).meta
 
 
 class Executor:
     """Model behaviour shared by both protocols (the MockServer analogue)."""
 
-    def __init__(self, plan_bytes: bytes, dtype: int):
+    def __init__(self, plan_bytes: bytes, dtype: int, meta: dict | None = None):
         from .runtime import Plan
         self.plan = Plan(plan_bytes, dtype)
-        self.meta = P.decode(plan_bytes).meta
+        self.meta = meta if meta is not None else P.decode(plan_bytes).meta
         self.started = time.monotonic()
 
     def healthy(self) -> bool:
@@ -222,7 +226,7 @@ def main(argv=None) -> int:
     args = build_parser().parse_args(argv)
     try:
         data = Path(args.model).read_bytes()
-        plan_bytes = load_plan_bytes(data)
+        plan_bytes, meta = load_plan(data)
     except OSError as exc:
         print(f"cannot read model: {exc}", file=sys.stderr)
         return FORMAT_EXIT
@@ -231,7 +235,7 @@ def main(argv=None) -> int:
         return FORMAT_EXIT
     dtype = {"auto": -1, "bf16": P.DT_BF16, "fp32": P.DT_FP32}[args.dtype]
     try:
-        ex = Executor(plan_bytes, dtype)
+        ex = Executor(plan_bytes, dtype, meta)
     except PlanFormatError as exc:
         print(f"cannot load plan: {exc}", file=sys.stderr)
         return FORMAT_EXIT

@@ -72,6 +72,14 @@ def main() -> int:
     prof = Profiler(hub, disp, tel, JobStore(hub.store))
     rows, cells, per_model = [], [], {}
     t_sweep = time.perf_counter()
+    # long-lived workers, started concurrently (process start, CUDA context and
+    # weight upload of the five models overlap instead of running in series)
+    import concurrent.futures as cf
+    with cf.ThreadPoolExecutor(len(models)) as ex:
+        futs = {m: ex.submit(disp.dispatch, variants[m][1], "gpu:0", "b200", "grpc-style")
+                for m in models}
+        warm = {m: f.result() for m, f in futs.items()}
+    prewarm_s = time.perf_counter() - t_sweep
     try:
         for m in models:
             rec, var = variants[m]
@@ -81,7 +89,7 @@ def main() -> int:
                                          requests_per_cell=args.requests,
                                          warmup_requests=args.warmup))
             tm = time.perf_counter()
-            res = prof.run_sweep(job)
+            res = prof.run_sweep(job, instance=warm[m])
             per_model[m] = {"wall_s": round(time.perf_counter() - tm, 3),
                             "failed_cells": list(job.failed_cells)}
             rows += res
@@ -95,8 +103,10 @@ def main() -> int:
     finally:
         disp.shutdown()
     wall = time.perf_counter() - t_sweep
-    setup = {m: max(0.0, per_model[m]["wall_s"] - sum(c["device_s"] for c in cells
-                                                      if c["model"] == m)) for m in models}
+    # per-model set-up on a GPU: its share of the concurrent worker start plus
+    # its cells' non-device time (graph capture, RPC)
+    setup = {m: prewarm_s / len(models) + max(0.0, per_model[m]["wall_s"] - sum(
+        c["device_s"] for c in cells if c["model"] == m)) for m in models}
     proj = {}
     for k in (1, 2, 4, 8):
         # each GPU runs its LPT share of cells; a model's worker start is paid on
@@ -111,7 +121,8 @@ def main() -> int:
     summary = {"config": "C4: " + ",".join(models) + " x batches " + args.batches,
                "requests_per_cell": args.requests, "warmup_requests": args.warmup,
                "gpus_measured": 1, "sweep_wall_s_measured": round(wall, 3),
-               "convert_s": round(convert_s, 3), "per_model": per_model,
+               "convert_s": round(convert_s, 3), "worker_prewarm_s": round(prewarm_s, 3),
+               "per_model": per_model,
                "sweep_wall_s_projected_lpt": proj,
                "projection": "LPT over measured per-cell device time + per-model worker "
                              "start/graph capture (measured wall - device time), one worker "
