@@ -279,9 +279,89 @@ __global__ void dwconv_vec_kernel(const T* __restrict__ x, const T* __restrict__
   *reinterpret_cast<uint4*>(y + ((b * OH + oh) * OW + ow) * (long)C + c0) = ov.u;
 }
 
+// 3x3 depthwise (MobileNetV2), stride 1 or 2, pad 1: the nine 16-byte input
+// loads and nine weight loads are all issued before any FMA (clamped
+// addresses, out-of-image taps masked), activation and stride compile-time.
+// The generic kernel's per-tap bounds branches serialised the loads.
+// (A strip-mined variant with a sliding 3-row register window — 3 loads per
+// output instead of 9 — measured slower: less parallelism, serial loads.)
+template <typename T, int STRIDE, int ACT>
+__global__ void __launch_bounds__(256) dwconv3_vec_kernel(const T* __restrict__ x,
+                                                          const T* __restrict__ w,
+                                                          const float* __restrict__ bias,
+                                                          T* __restrict__ y, int B, int H, int W,
+                                                          int C, int OH, int OW) {
+  constexpr int V = Vec16<T>::N;
+  const int CV = C / V;
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long total = (long)B * OH * OW * CV;
+  if (i >= total) return;
+  const int cv = (int)(i % CV);
+  long p = i / CV;
+  const int ow = (int)(p % OW);
+  p /= OW;
+  const int oh = (int)(p % OH);
+  const long b = p / OH;
+  const int c0 = cv * V;
+  Vec16<T> xv[9], wv[9];
+  bool ok[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int ih = oh * STRIDE - 1 + r;
+    const int ihc = min(max(ih, 0), H - 1);
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int iw = ow * STRIDE - 1 + s;
+      const int iwc = min(max(iw, 0), W - 1);
+      ok[r * 3 + s] = (unsigned)ih < (unsigned)H && (unsigned)iw < (unsigned)W;
+      xv[r * 3 + s].u = __ldg(reinterpret_cast<const uint4*>(x + ((b * H + ihc) * W + iwc) * C + c0));
+      wv[r * 3 + s].u = __ldg(reinterpret_cast<const uint4*>(w + (r * 3 + s) * C + c0));
+    }
+  }
+  float acc[V];
+  if (bias) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] = __ldg(bias + c0 + k);
+  } else {
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] = 0.f;
+  }
+#pragma unroll
+  for (int t = 0; t < 9; ++t)
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      acc[k] = ok[t] ? fmaf(to_f(xv[t].e[k]), to_f(wv[t].e[k]), acc[k]) : acc[k];
+  Vec16<T> ov;
+#pragma unroll
+  for (int k = 0; k < V; ++k) ov.e[k] = from_f<T>(act_t<ACT>(acc[k]));
+  *reinterpret_cast<uint4*>(y + ((b * OH + oh) * OW + ow) * (long)C + c0) = ov.u;
+}
+
+template <typename T, int STRIDE>
+static cudaError_t dwconv3_launch(const T* x, const T* w, const float* bias, T* y, int B, int H,
+                                  int W, int C, int OH, int OW, int act, cudaStream_t st) {
+  const long total = (long)B * OH * OW * (C / Vec16<T>::N);
+  switch (act) {
+#define B2_DW3(A)                                                                          \
+  case A:                                                                                  \
+    dwconv3_vec_kernel<T, STRIDE, A><<<nblk(total, 256), 256, 0, st>>>(x, w, bias, y, B, H, W, C, \
+                                                                       OH, OW);            \
+    return cudaGetLastError();
+    B2_DW3(ACT_NONE)
+    B2_DW3(ACT_RELU)
+    B2_DW3(ACT_RELU6)
+#undef B2_DW3
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <typename T>
 cudaError_t dwconv(const T* x, const T* w, const float* bias, T* y, int B, int H, int W, int C,
                    int R, int stride, int pad, int OH, int OW, int act, cudaStream_t st) {
+  if (C % Vec16<T>::N == 0 && R == 3 && pad == 1 && (stride == 1 || stride == 2) &&
+      (act == ACT_NONE || act == ACT_RELU || act == ACT_RELU6))
+    return stride == 1 ? dwconv3_launch<T, 1>(x, w, bias, y, B, H, W, C, OH, OW, act, st)
+                       : dwconv3_launch<T, 2>(x, w, bias, y, B, H, W, C, OH, OW, act, st);
   if (C % Vec16<T>::N == 0) {
     const long total = (long)B * OH * OW * (C / Vec16<T>::N);
     dwconv_vec_kernel<T><<<nblk(total, 256), 256, 0, st>>>(x, w, bias, y, B, H, W, C, R, stride,

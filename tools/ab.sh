@@ -1,4 +1,3 @@
 cd $GRAFT_REPO_ROOT
-for rep in 1 2; do for lib in ab/libb2_base.so paper_2006_05096_b200/libb2.so; do
-  B2_LIB=$PWD/$lib timeout 120 python tools/profile_ops.py bert 128 > gpurun_out/o.log 2>&1; echo "$lib $(head -1 gpurun_out/o.log)"; grep "N=3072" gpurun_out/o.log | head -2
-done; done
+timeout 300 python -m pytest tests/test_gpu.py -x -q -k "mobilenet" 2>&1 | tail -1
+timeout 120 python tools/profile_ops.py mobilenet_v2 256 > gpurun_out/ops_mb.log 2>&1; head -1 gpurun_out/ops_mb.log
