@@ -265,11 +265,25 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
         for (int kb = 0; kb < a.kblocks + a.res_kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (kb >= a.kblocks) {
-            // residual fold: A = res[m0:, n0 + j*64:], B = identity rows [0, BN)
             const int j = kb - a.kblocks;
             mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
-            tma_load_2d(sA + stage * Cfg::A_BYTES, &tmR, &full[stage], n0 + j * TC_BK, m0);
-            tma_load_2d(sB + stage * Cfg::B_BYTES, &tmI, &full[stage], j * TC_BK, 0);
+            if (a.fold_kind == 0) {
+              // residual fold: A = res[m0:, n0 + j*64:], B = identity rows [0, BN)
+              tma_load_2d(sA + stage * Cfg::A_BYTES, &tmR, &full[stage], n0 + j * TC_BK, m0);
+              tma_load_2d(sB + stage * Cfg::B_BYTES, &tmI, &full[stage], j * TC_BK, 0);
+            } else {
+              // folded projection shortcut: A = its input x, B = its weights
+              if (a.fold_kind == 1) {
+                tma_load_2d(sA + stage * Cfg::A_BYTES, &tmR, &full[stage], j * TC_BK, m0);
+              } else {
+                const int im = m0 / a.OHW;
+                const int rem = m0 - im * a.OHW;
+                const int oh = rem / a.OW;
+                tma_load_im2col_4d(sA + stage * Cfg::A_BYTES, &tmR, &full[stage], j * TC_BK,
+                                   (rem - oh * a.OW) * a.stride, oh * a.stride, im, 0, 0);
+              }
+              tma_load_2d(sB + stage * Cfg::B_BYTES, &tmI, &full[stage], j * TC_BK, n0);
+            }
           } else {
             if (GATHER) {
               mbar_arrive_expect_tx(&full[stage], Cfg::B_BYTES);

@@ -203,6 +203,7 @@ struct Layer {
   int s2d_shift = 0, s2d_H2 = 0, s2d_W2 = 0, s2d_Rp = 0, s2d_creal = 0;
   int im2col_mode = 0;      // TcArgs::a_im2col
   int pool_op = -1;         // s2d stem: index of the 3x3/s2 max-pool fused into its epilogue
+  int ds_op = -1;           // 1x1 conv: index of the projection shortcut folded into its K loop
   bool fused = false;       // max-pool executed inside its producer (no launch)
   int gmode = 0;            // see TcArgs::gmode
   int K = 0, kpad = 0, ldw = 0;
@@ -267,6 +268,7 @@ struct b2_plan {
   long pair_min_m = 4096;    // B2_PAIR_MIN_M: smallest M sent to the CTA-pair GEMM
   int pair_min_k = 1024;     // B2_PAIR_MIN_K: shortest K sent to the CTA-pair GEMM
   bool use_pool_fusion = true;   // B2_POOL_FUSION=0 -> stem and max-pool as two kernels
+  bool use_ds_fold = true;       // B2_DS_FOLD=0 -> projection shortcuts as their own kernels
   int band_max_n = 128;      // B2_BAND_MAX_N: widest conv (output channels) sent to conv_band
   void* identity = nullptr;  // bf16 I[256][256]
   void* stage = nullptr;     // weight-upload staging (plan creation only)
@@ -397,6 +399,49 @@ void plan_fuse_pool(b2_plan* pl) {
   }
 }
 
+// Fold a ResNet projection shortcut into the block's last 1x1 conv:
+//   out = act(t2 W3^T + b3 + x Wd^T + bd)
+// computed as one GEMM over K = [t2 | x (strided)] with B = [W3 | Wd], so the
+// shortcut's output (411 MB at layer1, b=256) is neither written nor read
+// back as a residual, and its kernel disappears.  Conditions: the shortcut
+// is a plain 1x1 conv (pad 0, stride 1 or 2, no activation/residual) whose
+// output feeds only this conv's residual input, channels multiples of 64.
+void plan_fold_downsample(b2_plan* pl) {
+  if (pl->dtype != B2_DT_BF16 || pl->force_simt || !pl->use_ds_fold) return;
+  auto users = [&](int t) {
+    int n = 0;
+    for (const Layer& Lj : pl->layers) {
+      if (Lj.kind == OP_OUTPUT) {
+        for (int q = 0; q < Lj.p[0]; ++q) n += Lj.p[1 + 2 * q] == t;
+      } else if (Lj.kind != OP_INPUT && Lj.kind != OP_TOKENS) {
+        n += Lj.p[0] == t;
+        n += (Lj.kind == OP_CONV && Lj.p[15] == t) || (Lj.kind == OP_LINEAR && Lj.p[8] == t) ||
+             (Lj.kind == OP_LAYERNORM && Lj.p[7] == t);
+      }
+    }
+    return n;
+  };
+  for (size_t ci = 0; ci < pl->layers.size(); ++ci) {
+    Layer& C3 = pl->layers[ci];
+    const int* p = C3.p;
+    if (C3.kind != OP_CONV || p[15] < 0 || p[8] != 1 || p[9] != 1 || p[10] != 1 || p[11] != 0 ||
+        p[7] % 64 != 0 || p[6] % 64 != 0)
+      continue;
+    for (size_t di = 0; di < pl->layers.size(); ++di) {
+      Layer& D = pl->layers[di];
+      const int* q = D.p;
+      if (di == ci || D.kind != OP_CONV || q[1] != p[15] || q[8] != 1 || q[9] != 1 || q[11] != 0 ||
+          (q[10] != 1 && q[10] != 2) || q[14] != ACT_NONE || q[15] >= 0 || q[6] % 64 != 0 ||
+          q[7] != p[7] || q[12] != p[12] || q[13] != p[13] || users(p[15]) != 1)
+        continue;
+      C3.ds_op = (int)di;
+      D.fused = true;
+      pl->virt[p[15]] = 1;
+      break;
+    }
+  }
+}
+
 int upload_weights(b2_plan* pl, const uint8_t* data, const std::vector<WeightRec>& wr,
                    size_t data_len) {
   const bool bf = pl->dtype == B2_DT_BF16;
@@ -417,7 +462,17 @@ int upload_weights(b2_plan* pl, const uint8_t* data, const std::vector<WeightRec
         const int K = conv ? L.p[8] * L.p[9] * L.p[6] : L.p[4];
         const float* w = wptr(L.p[2], &n);
         if (!w || n != (size_t)N * K) return fail(B2_ERR_FORMAT, "weight %d size mismatch", L.p[2]);
-        if (L.p[3] >= 0) {
+        if (L.ds_op >= 0) {
+          // folded projection shortcut: one bias b3 + bd
+          std::vector<float> bsum(N, 0.f);
+          for (int src : {L.p[3], pl->layers[L.ds_op].p[3]}) {
+            if (src < 0) continue;
+            const float* bsrc = wptr(src, &nb);
+            if (!bsrc || nb != (size_t)N) return fail(B2_ERR_FORMAT, "bias size mismatch");
+            for (int j = 0; j < N; ++j) bsum[j] += bsrc[j];
+          }
+          if ((rc = upload_f32(pl, bsum.data(), bsum.size(), &L.bias))) return rc;
+        } else if (L.p[3] >= 0) {
           const float* bsrc = wptr(L.p[3], &nb);
           if (!bsrc || nb != (size_t)N) return fail(B2_ERR_FORMAT, "bias size mismatch");
           if ((rc = upload_f32(pl, bsrc, nb, &L.bias))) return rc;
@@ -602,6 +657,7 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
         break;
       case OP_CONV:
       case OP_LINEAR: {
+        if (L.fused) break;   // projection shortcut folded into the block's last conv
         const bool conv = L.kind == OP_CONV;
         const int N = conv ? p[7] : p[5];
         const long M = conv ? (long)B * p[12] * p[13] : (long)B * p[6];
@@ -658,6 +714,16 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
           a.ts_debug = pl->ts_debug;
           a.stages = pl->stages_override;
           a.res_kblocks = S.fold[li] ? bn / 64 : 0;
+          if (S.fold[li] >= 2) {
+            const int* q = pl->layers[L.ds_op].p;
+            a.res_kblocks = pl->layers[L.ds_op].kpad / 64;
+            a.fold_kind = S.fold[li] - 1;   // 1: stride-1 shortcut, 2: strided (im2col)
+            a.ds_H = q[4];
+            a.ds_W = q[5];
+            a.OW = q[13];
+            a.OHW = q[12] * q[13];
+            a.stride = q[10];
+          }
           if (S.pair[li]) {
             a.tiles_m = (int)((M + 255) / 256);
             CK(tc_gemm2_launch(a, bn, S.tmA[li], S.tmB[li], S.tmO[li],
@@ -915,7 +981,8 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     // measured (tools/gemm_sweep.sh): pairs win on long-K, wide-N GEMMs
     // (K >= 1024, BN = 256: +7% at 16384x4096x4096, +7% at 50176x1024x256)
     // and lose on short-K / residual-fold / BN = 128 shapes
-    const bool pair_ok = pl->use_pair && !L.s2d && !L.gather && (!L.im2col || L.im2col_mode == 1) &&
+    const bool pair_ok = pl->use_pair && !L.s2d && !L.gather && L.ds_op < 0 &&
+                         (!L.im2col || L.im2col_mode == 1) &&
                          N % 8 == 0 && M >= pl->pair_min_m && L.K >= pl->pair_min_k &&
                          tc2_pick_bn(M, N, pl->num_sms) == 256;
     int bn = pair_ok ? tc2_pick_bn(M, N, pl->num_sms) : tc_pick_bn(M, N, pl->num_sms);
@@ -961,7 +1028,22 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     // residual fold: cheap in MMA time when K is small, and it moves the
     // residual read out of the epilogue into the TMA pipeline
     const int res_t = conv ? p[15] : p[8];
-    if (res_t >= 0 && bn >= 64 && N % 8 == 0 && L.K <= pl->fold_max_k && pl->identity) {
+    if (L.ds_op >= 0) {
+      // folded shortcut: A = its input x (2D for stride 1, im2col for stride 2),
+      // B = its weights; K blocks appended after this conv's own
+      const Layer& D = pl->layers[L.ds_op];
+      const int* q = D.p;
+      bool ok;
+      if (q[10] == 1)
+        ok = make_tmap_bf16(&S.tmR[li], S.act[q[0]], (uint64_t)M, (uint64_t)q[6],
+                            (uint64_t)q[6] * 2, 128);
+      else
+        ok = make_tmap_im2col(&S.tmR[li], S.act[q[0]], batch, q[4], q[5], q[6], 1, 1, q[10], 0, 64);
+      if (!ok || !make_tmap_bf16(&S.tmI[li], D.w, (uint64_t)N, (uint64_t)D.kpad,
+                                 (uint64_t)D.kpad * 2, bbox))
+        return fail(B2_ERR_CUDA, "layer %zu: folded shortcut tensor maps rejected", li);
+      S.fold[li] = q[10] == 1 ? 2 : 3;
+    } else if (res_t >= 0 && bn >= 64 && N % 8 == 0 && L.K <= pl->fold_max_k && pl->identity) {
       if (!make_tmap_bf16(&S.tmR[li], S.act[res_t], (uint64_t)M, (uint64_t)N, (uint64_t)N * 2,
                           128) ||
           !make_tmap_bf16(&S.tmI[li], pl->identity, 256, 256, 512, bbox))
@@ -1086,6 +1168,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* pm = getenv("B2_PAIR_MIN_M")) pl->pair_min_m = atol(pm);
   if (const char* pk = getenv("B2_PAIR_MIN_K")) pl->pair_min_k = atoi(pk);
   if (const char* pf = getenv("B2_POOL_FUSION")) pl->use_pool_fusion = pf[0] != '0';
+  if (const char* df = getenv("B2_DS_FOLD")) pl->use_ds_fold = df[0] != '0';
   if (const char* bm = getenv("B2_BAND_MAX_N")) pl->band_max_n = atoi(bm);
   cudaGetDevice(&pl->device);
   cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, pl->device);
@@ -1119,6 +1202,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   int rc = validate_ops(pl);
   if (!rc) plan_s2d(pl);
   if (!rc) plan_fuse_pool(pl);
+  if (!rc) plan_fold_downsample(pl);
   if (!rc) rc = upload_weights(pl, d + pos, wr, len - 4 - pos);
   if (!rc && pl->dtype == B2_DT_BF16) {
     std::vector<float> eye(256 * 256, 0.f);

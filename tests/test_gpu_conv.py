@@ -171,3 +171,54 @@ def test_gemm_shapes(gpu_required, monkeypatch, M, K, N, res, pair):
 ])
 def test_late_convs(gpu_required, H, C, N, k, stride, batch):
     check(conv_plan(H, H, C, N, k, stride), batch)
+
+
+def shortcut_plan(H, C, Cm, N, stride, seed=0):
+    """Bottleneck tail with a projection shortcut:
+    t = relu(conv3x3/stride(x)); out = relu(conv1x1(t) + conv1x1/stride(x))."""
+    b = P.PlanBuilder("shortcut")
+    x = b.tensor(H, H, C)
+    b.in_elems = C * H * H
+    b.op_p(P.OP_INPUT, [x, C, H, H, C])
+    rng = np.random.default_rng(seed)
+    OH = (H + 2 - 3) // stride + 1
+    t = b.tensor(OH, OH, Cm)
+    b.op_p(P.OP_CONV, [x, t, b.weight(rng.standard_normal((Cm, 3, 3, C)) / np.sqrt(9 * C)),
+                       b.weight(rng.standard_normal(Cm) * 0.1), H, H, C, Cm, 3, 3, stride, 1,
+                       OH, OH, 1, -1])
+    d = b.tensor(OH, OH, N)
+    b.op_p(P.OP_CONV, [x, d, b.weight(rng.standard_normal((N, 1, 1, C)) / np.sqrt(C)),
+                       b.weight(rng.standard_normal(N) * 0.1), H, H, C, N, 1, 1, stride, 0,
+                       OH, OH, 0, -1])
+    y = b.tensor(OH, OH, N)
+    b.op_p(P.OP_CONV, [t, y, b.weight(rng.standard_normal((N, 1, 1, Cm)) / np.sqrt(Cm)),
+                       b.weight(rng.standard_normal(N) * 0.1), OH, OH, Cm, N, 1, 1, 1, 0,
+                       OH, OH, 1, d])
+    b.out_elems = b.tensors[y].elems
+    b.op_p(P.OP_OUTPUT, [1, y, 0])
+    return b.build(P.DT_FP32)
+
+
+@pytest.mark.parametrize("H,C,Cm,N,stride,batch", [
+    (56, 64, 64, 256, 1, 6),      # ResNet layer1 block 0
+    (56, 256, 128, 512, 2, 4),    # layer2 block 0 (strided shortcut via im2col TMA)
+    (14, 1024, 512, 2048, 2, 8),  # layer4 block 0
+])
+@pytest.mark.parametrize("fold", ["1", "0"])
+def test_shortcut_fold(gpu_required, monkeypatch, H, C, Cm, N, stride, batch, fold):
+    """Projection shortcut folded into the block's last 1x1 conv (its output is
+    never materialised; read_tensor reports it fused) vs run as its own conv."""
+    monkeypatch.setenv("B2_DS_FOLD", fold)
+    blob = shortcut_plan(H, C, Cm, N, stride)
+    pl = P.decode(blob)
+    x = plan_ref.make_inputs(pl, batch, 9)
+    plan = R.Plan(blob, P.DT_BF16)
+    try:
+        out = plan.predict(x)
+        assert np.isfinite(out).all()
+        rt = lambda t: plan.read_tensor(batch, t, pl.tensors[t].elems, pl.tensors[t].kind)
+        assert (rt(pl.ops[2][1]) is None) == (fold == "1")
+        errs = plan_ref.layerwise_errors(pl, rt, x, True)
+        assert errs and all(e[2] <= TOL for e in errs), errs
+    finally:
+        plan.close()
