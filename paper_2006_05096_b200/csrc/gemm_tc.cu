@@ -64,6 +64,14 @@ B2_DEV void add_bf16x8(float* v, const uint4& u) {
 
 // TMA-store epilogue of one warp, specialised on the activation so the
 // per-element math is branch-free.
+// M tile of linear tile index t.  Consecutive layers alternate the M
+// direction (a.reverse): the next kernel then starts on the rows its producer
+// wrote last, which are still in L2.
+B2_DEV int mtile_of(const TcArgs& a, int t) {
+  const int mt = t / a.tiles_n;
+  return a.reverse ? a.tiles_m - 1 - mt : mt;
+}
+
 // Tiles t = t0, t0 + tstep, ... < ntiles; tile t covers rows
 // (t / tiles_n) * mstride + mofs.  `tempty_remote` != 0: signal accumulator
 // release on the CTA-pair leader's barrier (cluster address) instead of ours.
@@ -83,7 +91,7 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint
   for (int t = t0; t < ntiles; t += tstep, ++it) {
     const int as = it & 1;
     const uint32_t aph = (it >> 1) & 1;
-    const int m0 = (t / a.tiles_n) * mstride + mofs;
+    const int m0 = mtile_of(a, t) * mstride + mofs;
     const int n0 = (t % a.tiles_n) * BN;
     const int row0 = m0 + lg * 32;
     const int row = row0 + lane;
@@ -252,7 +260,7 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
       uint32_t phase = 0;
       const int cpb = a.C >> 6;   // im2col: 64-channel K blocks per filter tap
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int m0 = (t / a.tiles_n) * TC_BM;
+        const int m0 = mtile_of(a, t) * TC_BM;
         const int n0 = (t % a.tiles_n) * BN;
         int iw0 = 0, ih0 = 0, img = 0;
         if (!GATHER && a.a_im2col) {
@@ -405,7 +413,7 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int as = it & 1;
         const uint32_t aph = (it >> 1) & 1;
-        const int m0 = (t / a.tiles_n) * TC_BM;
+        const int m0 = mtile_of(a, t) * TC_BM;
         const int n0 = (t % a.tiles_n) * BN;
         mbar_wait(&tfull[as], aph);
         tc_fence_after();
@@ -475,7 +483,7 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
     uint32_t phase = 0;
     const size_t img_elems = (size_t)a.H * a.W * a.C;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int m = (t / a.tiles_n) * TC_BM + g;
+      const int m = mtile_of(a, t) * TC_BM + g;
       const bool vrow = m < a.M;
       int img = 0, oh = 0, ow = 0;
       if (vrow) {
@@ -661,7 +669,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<BN>::THREADS,
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cid; t < ntiles; t += ncl) {
-        const int m0 = (t / a.tiles_n) * (2 * TC_BM) + (int)rank * TC_BM;
+        const int m0 = mtile_of(a, t) * (2 * TC_BM) + (int)rank * TC_BM;
         const int n0 = (t % a.tiles_n) * BN;
         const int nb = n0 + (int)rank * (BN / 2);          // this CTA's half of the weights
         int iw0 = 0, ih0 = 0, img = 0;

@@ -40,6 +40,7 @@ struct TcArgs {
                         // 1 = 64-channel im2col boxes (C % 64 == 0, 128B swizzle);
                         // 2 = one 8-channel filter tap per 2 KB box (C == 8 stems), 8 taps
                         //     per K block in the non-swizzled K-major layout
+  int reverse;          // walk M tiles last-to-first (L2 reuse across layers)
   int fold_kind;        // extra K blocks: 0 residual x identity; 1 shortcut x (stride 1, 2D)
                         // against its weights; 2 strided shortcut x (im2col TMA)
   int ds_H, ds_W;       // fold_kind 2: shortcut input geometry (uses OW, OHW, stride too)

@@ -269,6 +269,7 @@ struct b2_plan {
   int pair_min_k = 1024;     // B2_PAIR_MIN_K: shortest K sent to the CTA-pair GEMM
   bool use_pool_fusion = true;   // B2_POOL_FUSION=0 -> stem and max-pool as two kernels
   bool use_ds_fold = true;       // B2_DS_FOLD=0 -> projection shortcuts as their own kernels
+  bool alt_order = true;         // B2_ALT_ORDER=0 -> every GEMM walks M tiles forward
   int band_max_n = 128;      // B2_BAND_MAX_N: widest conv (output channels) sent to conv_band
   void* identity = nullptr;  // bf16 I[256][256]
   void* stage = nullptr;     // weight-upload staging (plan creation only)
@@ -713,6 +714,7 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
           a.epi_debug = pl->epi_mode == 2 ? 0 : pl->epi_mode;
           a.ts_debug = pl->ts_debug;
           a.stages = pl->stages_override;
+          a.reverse = pl->alt_order ? (launches & 1) : 0;
           a.res_kblocks = S.fold[li] ? bn / 64 : 0;
           if (S.fold[li] >= 2) {
             const int* q = pl->layers[L.ds_op].p;
@@ -1169,6 +1171,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* pk = getenv("B2_PAIR_MIN_K")) pl->pair_min_k = atoi(pk);
   if (const char* pf = getenv("B2_POOL_FUSION")) pl->use_pool_fusion = pf[0] != '0';
   if (const char* df = getenv("B2_DS_FOLD")) pl->use_ds_fold = df[0] != '0';
+  if (const char* ao = getenv("B2_ALT_ORDER")) pl->alt_order = ao[0] != '0';
   if (const char* bm = getenv("B2_BAND_MAX_N")) pl->band_max_n = atoi(bm);
   cudaGetDevice(&pl->device);
   cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, pl->device);
