@@ -76,6 +76,24 @@ cudaError_t conv_band_launch(const BandArgs& a, int bn, int cgw, const CUtensorM
                              const CUtensorMap& tb, const CUtensorMap& to, int num_sms,
                              cudaStream_t st);
 
+// ---- chained 1x1 convs (chain_tc.cu): block tail conv -> next block's conv1 --
+struct ChainArgs {
+  int M, N1, N2;        // O = relu(A W3^T + b1 + fold) [M, N1]; T1 = relu(O W1^T + b2) [M, N2]
+  int kblocks;          // K1 / 64
+  int res_kblocks;      // fold K blocks per 128-column O chunk
+  int fold_kind;        // 0 residual x identity; 1 shortcut x (2D); 2 strided shortcut (im2col)
+  int OW, OHW, stride;  // fold_kind 2 geometry
+  int tiles_m, reverse;
+  int stages, b2_stages;   // set by chain_config
+  const float* bias1;
+  const float* bias2;
+};
+bool chain_config(ChainArgs& a);
+cudaError_t chain_launch(const ChainArgs& a, const CUtensorMap& tA, const CUtensorMap& tB1,
+                         const CUtensorMap& tR, const CUtensorMap& tI, const CUtensorMap& tB2,
+                         const CUtensorMap& tO, const CUtensorMap& tT, int num_sms,
+                         cudaStream_t st);
+
 int tc_pick_bn(long M, int N, int num_sms);
 int tc2_pick_bn(long M, int N, int num_sms);
 cudaError_t tc_gemm2_launch(const TcArgs& a, int bn, const CUtensorMap& ta, const CUtensorMap& tb,

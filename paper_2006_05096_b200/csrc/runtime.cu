@@ -204,6 +204,7 @@ struct Layer {
   int im2col_mode = 0;      // TcArgs::a_im2col
   int pool_op = -1;         // s2d stem: index of the 3x3/s2 max-pool fused into its epilogue
   int ds_op = -1;           // 1x1 conv: index of the projection shortcut folded into its K loop
+  int chain_op = -1;        // block-tail 1x1 conv: next block's 1x1 conv computed in the same kernel
   bool fused = false;       // max-pool executed inside its producer (no launch)
   int gmode = 0;            // see TcArgs::gmode
   int K = 0, kpad = 0, ldw = 0;
@@ -224,6 +225,9 @@ struct BatchState {
   std::vector<CUtensorMap> tmI;    // per layer: identity [256 x 256] (box rows = BN) for the fold
   std::vector<char> band;          // per layer: banded implicit-GEMM conv (conv_band.cu)
   std::vector<char> pair;          // per layer: CTA-pair GEMM (tc_gemm2_kernel)
+  std::vector<char> chain;         // per layer: chained with the next conv1 (chain_tc.cu)
+  std::vector<ChainArgs> cargs;
+  std::vector<CUtensorMap> tmB2, tmT;   // chain: second weights, second output
   std::vector<BandArgs> bargs;     // per layer (band): geometry chosen by band_config
   cudaGraphExec_t graph = nullptr;
   void* h_in = nullptr;            // pinned (e2e)
@@ -270,6 +274,7 @@ struct b2_plan {
   bool use_pool_fusion = true;   // B2_POOL_FUSION=0 -> stem and max-pool as two kernels
   bool use_ds_fold = true;       // B2_DS_FOLD=0 -> projection shortcuts as their own kernels
   bool alt_order = true;         // B2_ALT_ORDER=0 -> every GEMM walks M tiles forward
+  bool use_chain = true;         // B2_CHAIN=0 -> block-tail and next conv1 as two GEMMs
   int band_max_n = 128;      // B2_BAND_MAX_N: widest conv (output channels) sent to conv_band
   void* identity = nullptr;  // bf16 I[256][256]
   void* stage = nullptr;     // weight-upload staging (plan creation only)
@@ -438,6 +443,37 @@ void plan_fold_downsample(b2_plan* pl) {
       C3.ds_op = (int)di;
       D.fused = true;
       pl->virt[p[15]] = 1;
+      break;
+    }
+  }
+}
+
+// Chain a block's last 1x1 conv (O = relu(t2 W3^T + b3 + residual or folded
+// shortcut)) with the next block's first 1x1 conv (T1 = relu(O W1^T + b1)) in
+// one kernel (chain_tc.cu): O is written once and consumed from shared
+// memory.  Needs 128 | N1, 64 | N2 <= 256.
+void plan_chain(b2_plan* pl) {
+  if (pl->dtype != B2_DT_BF16 || pl->force_simt || !pl->use_chain) return;
+  for (size_t ci = 0; ci < pl->layers.size(); ++ci) {
+    Layer& C3 = pl->layers[ci];
+    const int* p = C3.p;
+    if (C3.kind != OP_CONV || C3.fused || p[15] < 0 || p[8] != 1 || p[9] != 1 || p[10] != 1 ||
+        p[11] != 0 || p[14] != ACT_RELU || p[6] % 64 != 0 || p[7] % 128 != 0)
+      continue;
+    for (size_t j = ci + 1; j < pl->layers.size(); ++j) {
+      Layer& C1 = pl->layers[j];
+      const int* q = C1.p;
+      if (C1.kind != OP_CONV || C1.fused || q[0] != p[1] || q[8] != 1 || q[9] != 1 || q[10] != 1 ||
+          q[11] != 0 || q[14] != ACT_RELU || q[15] >= 0 || q[7] % 64 != 0 || q[7] > 256 ||
+          q[6] != p[7])
+        continue;
+      // measured (ResNet-50 b=256, per-op events): the chain wins where both
+      // GEMMs are HBM-bound (N1 = 256: -30 us per block; N1 = 512 with
+      // N2 = 128: -8..-22 us) and loses once they are operand-bound (N1 = 1024:
+      // +24..+89 us — every 128-column chunk re-reads its A panel)
+      if (!(p[7] <= 256 || (p[7] <= 512 && q[7] <= 128))) break;
+      C3.chain_op = (int)j;
+      C1.fused = true;
       break;
     }
   }
@@ -665,7 +701,12 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
         const int res_t = conv ? p[15] : p[8];
         const int act = conv ? p[14] : p[7];
         T* out = A(p[1]);
-        if (L.tc && S.band[li] && L.pool_op >= 0) {
+        if (L.tc && S.chain[li]) {
+          ChainArgs ca = S.cargs[li];
+          ca.reverse = pl->alt_order ? (launches & 1) : 0;
+          CK(chain_launch(ca, S.tmA[li], S.tmB[li], S.tmR[li], S.tmI[li], S.tmB2[li], S.tmO[li],
+                          S.tmT[li], pl->num_sms, st));
+        } else if (L.tc && S.band[li] && L.pool_op >= 0) {
           CK(stem_pool_launch(S.bargs[li], S.tmA[li], S.tmB[li], pl->num_sms, st));
         } else if (L.tc && S.band[li]) {
           CK(conv_band_launch(S.bargs[li], S.bn[li], L.s2d ? 16 : 64, S.tmA[li], S.tmB[li],
@@ -832,6 +873,63 @@ size_t in_bytes(const b2_plan* pl, int batch) {
   return (size_t)batch * pl->in_elems * (pl->input_kind == B2_IN_TOKENS_I64 ? 8 : 4);
 }
 
+// Tensor maps and arguments of a chained block tail (plan_chain).  Returns 1
+// when set up, -code on error.
+int plan_chain_state(b2_plan* pl, BatchState& S, size_t li, int batch) {
+  Layer& L = pl->layers[li];
+  if (L.chain_op < 0) return 0;
+  const int* p = L.p;
+  const Layer& C1 = pl->layers[L.chain_op];
+  const int N1 = p[7], N2 = C1.p[7];
+  const long M = (long)batch * p[12] * p[13];
+  ChainArgs a{};
+  a.M = (int)M;
+  a.N1 = N1;
+  a.N2 = N2;
+  a.kblocks = L.kpad / 64;
+  a.tiles_m = (int)((M + 127) / 128);
+  a.bias1 = L.bias ? L.bias : pl->zero_bias;
+  a.bias2 = C1.bias ? C1.bias : pl->zero_bias;
+  bool ok = make_tmap_bf16(&S.tmA[li], S.act[p[0]], (uint64_t)M, (uint64_t)L.K,
+                           (uint64_t)p[6] * 2, 128) &&
+            make_tmap_bf16(&S.tmB[li], L.w, (uint64_t)N1, (uint64_t)L.kpad, (uint64_t)L.kpad * 2,
+                           128) &&
+            make_tmap_bf16(&S.tmB2[li], C1.w, (uint64_t)N2, (uint64_t)C1.kpad,
+                           (uint64_t)C1.kpad * 2, (uint32_t)N2) &&
+            make_tmap_bf16(&S.tmO[li], S.act[p[1]], (uint64_t)M, (uint64_t)N1, (uint64_t)N1 * 2,
+                           128) &&
+            make_tmap_bf16(&S.tmT[li], S.act[C1.p[1]], (uint64_t)M, (uint64_t)N2,
+                           (uint64_t)N2 * 2, 128);
+  if (L.ds_op >= 0) {
+    const Layer& D = pl->layers[L.ds_op];
+    const int* q = D.p;
+    if (q[10] == 1)
+      ok = ok && make_tmap_bf16(&S.tmR[li], S.act[q[0]], (uint64_t)M, (uint64_t)q[6],
+                                (uint64_t)q[6] * 2, 128);
+    else
+      ok = ok && make_tmap_im2col(&S.tmR[li], S.act[q[0]], batch, q[4], q[5], q[6], 1, 1, q[10],
+                                  0, 64);
+    ok = ok && make_tmap_bf16(&S.tmI[li], D.w, (uint64_t)N1, (uint64_t)D.kpad,
+                              (uint64_t)D.kpad * 2, 128);
+    a.res_kblocks = D.kpad / 64;
+    a.fold_kind = q[10] == 1 ? 1 : 2;
+    a.OW = q[13];
+    a.OHW = q[12] * q[13];
+    a.stride = q[10];
+  } else {
+    ok = ok && make_tmap_bf16(&S.tmR[li], S.act[p[15]], (uint64_t)M, (uint64_t)N1,
+                              (uint64_t)N1 * 2, 128) &&
+         make_tmap_bf16(&S.tmI[li], pl->identity, 256, 256, 512, 128);
+    a.res_kblocks = 2;             // 128 residual columns per O chunk
+    a.fold_kind = 0;
+  }
+  if (!ok) return -fail(B2_ERR_CUDA, "layer %zu: chain tensor maps rejected", li);
+  if (!chain_config(a)) return -fail(B2_ERR_UNSUPPORTED, "layer %zu: chain does not fit", li);
+  S.chain[li] = 1;
+  S.cargs[li] = a;
+  return 1;
+}
+
 // Banded implicit-GEMM conv (conv_band.cu) for stride-1 "same" k x k convs
 // with C % 64 == 0 and for space-to-depth stems.  Returns 1 when layer li
 // runs banded (tensor maps built), 0 to keep the gemm_tc path, -code on error.
@@ -961,12 +1059,19 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
   S.tmI.resize(pl->layers.size());
   S.band.assign(pl->layers.size(), 0);
   S.pair.assign(pl->layers.size(), 0);
+  S.chain.assign(pl->layers.size(), 0);
+  S.cargs.resize(pl->layers.size());
+  S.tmB2.resize(pl->layers.size());
+  S.tmT.resize(pl->layers.size());
   S.bargs.resize(pl->layers.size());
   for (size_t li = 0; li < pl->layers.size(); ++li) {
     Layer& L = pl->layers[li];
     if (!L.tc) continue;
     const int* p = L.p;
     int brc = plan_band(pl, S, li, batch);
+    if (brc < 0) return -brc;
+    if (brc == 1) continue;
+    brc = plan_chain_state(pl, S, li, batch);
     if (brc < 0) return -brc;
     if (brc == 1) continue;
     if (L.kind == OP_ATTENTION) {
@@ -1172,6 +1277,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* pf = getenv("B2_POOL_FUSION")) pl->use_pool_fusion = pf[0] != '0';
   if (const char* df = getenv("B2_DS_FOLD")) pl->use_ds_fold = df[0] != '0';
   if (const char* ao = getenv("B2_ALT_ORDER")) pl->alt_order = ao[0] != '0';
+  if (const char* cz = getenv("B2_CHAIN")) pl->use_chain = cz[0] != '0';
   if (const char* bm = getenv("B2_BAND_MAX_N")) pl->band_max_n = atoi(bm);
   cudaGetDevice(&pl->device);
   cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, pl->device);
@@ -1206,6 +1312,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (!rc) plan_s2d(pl);
   if (!rc) plan_fuse_pool(pl);
   if (!rc) plan_fold_downsample(pl);
+  if (!rc) plan_chain(pl);
   if (!rc) rc = upload_weights(pl, d + pos, wr, len - 4 - pos);
   if (!rc && pl->dtype == B2_DT_BF16) {
     std::vector<float> eye(256 * 256, 0.f);

@@ -222,3 +222,58 @@ def test_shortcut_fold(gpu_required, monkeypatch, H, C, Cm, N, stride, batch, fo
         assert errs and all(e[2] <= TOL for e in errs), errs
     finally:
         plan.close()
+
+
+def chain_plan(H, C, Cm, N1, N2, shortcut, seed=0):
+    """Block tail + next block's first conv:
+    t = relu(conv1x1(x, C->Cm)); O = relu(conv1x1(t, Cm->N1) + R);
+    T1 = relu(conv1x1(O, N1->N2)); R = x (identity, C == N1) or a 1x1
+    projection of x (shortcut=1) / strided by 2 (shortcut=2, t from a 3x3/2)."""
+    b = P.PlanBuilder("chain")
+    x = b.tensor(H, H, C)
+    b.in_elems = C * H * H
+    b.op_p(P.OP_INPUT, [x, C, H, H, C])
+    rng = np.random.default_rng(seed)
+    st = 2 if shortcut == 2 else 1
+    OH = H // st
+    k = 3 if shortcut == 2 else 1
+    t = b.tensor(OH, OH, Cm)
+    b.op_p(P.OP_CONV, [x, t, b.weight(rng.standard_normal((Cm, k, k, C)) / np.sqrt(k * k * C)),
+                       b.weight(rng.standard_normal(Cm) * 0.1), H, H, C, Cm, k, k, st, k // 2,
+                       OH, OH, 1, -1])
+    if shortcut:
+        r = b.tensor(OH, OH, N1)
+        b.op_p(P.OP_CONV, [x, r, b.weight(rng.standard_normal((N1, 1, 1, C)) / np.sqrt(C)),
+                           b.weight(rng.standard_normal(N1) * 0.1), H, H, C, N1, 1, 1, st, 0,
+                           OH, OH, 0, -1])
+    else:
+        r = x
+    o = b.tensor(OH, OH, N1)
+    b.op_p(P.OP_CONV, [t, o, b.weight(rng.standard_normal((N1, 1, 1, Cm)) / np.sqrt(Cm)),
+                       b.weight(rng.standard_normal(N1) * 0.1), OH, OH, Cm, N1, 1, 1, 1, 0,
+                       OH, OH, 1, r])
+    t1 = b.tensor(OH, OH, N2)
+    b.op_p(P.OP_CONV, [o, t1, b.weight(rng.standard_normal((N2, 1, 1, N1)) / np.sqrt(N1)),
+                       b.weight(rng.standard_normal(N2) * 0.1), OH, OH, N1, N2, 1, 1, 1, 0,
+                       OH, OH, 1, -1])
+    b.out_elems = b.tensors[o].elems + b.tensors[t1].elems
+    b.op_p(P.OP_OUTPUT, [2, o, 0, t1, b.tensors[o].elems])
+    return b.build(P.DT_FP32)
+
+
+@pytest.mark.parametrize("H,C,Cm,N1,N2,shortcut,batch", [
+    (56, 256, 64, 256, 64, 0, 3),      # layer1 blocks 1-2: identity residual, 2 O chunks
+    (56, 64, 64, 256, 64, 1, 2),       # layer1 block 0: projection shortcut (stride 1)
+    (28, 512, 128, 512, 128, 0, 5),    # layer2: 4 O chunks, N2 = 128
+    (28, 256, 128, 512, 128, 2, 4),    # layer2 block 0: strided shortcut (im2col)
+    (14, 1024, 256, 1024, 256, 0, 9),  # layer3: 8 O chunks, N2 = 256
+    (9, 128, 64, 128, 192, 0, 7),      # one O chunk, N2 = 192, ragged M
+])
+@pytest.mark.parametrize("chain", ["1", "0"])
+def test_chain(gpu_required, monkeypatch, H, C, Cm, N1, N2, shortcut, batch, chain):
+    """Chained block tail + next conv1 (chain_tc.cu) against the oracle, both
+    layerwise and end to end on the two outputs; and the unchained path."""
+    if shortcut == 0 and C != N1:
+        pytest.skip("identity residual needs C == N1")
+    monkeypatch.setenv("B2_CHAIN", chain)
+    check(chain_plan(H, C, Cm, N1, N2, shortcut), batch)
