@@ -53,10 +53,17 @@ B2_DEV uint64_t smem_desc_sw32(uint32_t smem_addr) {
   return d;
 }
 
+// CGW = 8 (3-channel image inputs padded to 8): the band is a plain array of
+// 16-byte pixels (no swizzle).  One K = 16 UMMA step covers TWO horizontally
+// adjacent taps: in the non-swizzled K-major layout, core matrix 0 (K 0-7) is
+// pixels p..p+7 and core matrix 1 (K 8-15) is pixels p+1..p+8, i.e. LBO = 16 B
+// and SBO = 128 B over the same bytes.  Weights are laid out [N][r][4 taps][8]
+// with the fourth tap zero, so a 3x3 conv is 6 UMMA steps per M tile.
 template <int CGW>
 B2_DEV uint64_t band_adesc(uint32_t addr) {
   if constexpr (CGW == 64) return smem_desc_sw128(addr);
-  else return smem_desc_sw32(addr);
+  else if constexpr (CGW == 16) return smem_desc_sw32(addr);
+  else return smem_desc_kmajor_noswizzle(addr, 16, 128);
 }
 
 // R x S taps and B residency are compile-time so the MMA issue loop unrolls
@@ -68,9 +75,10 @@ template <int BN, int CGW, int R, int S, bool BRES, int ACT>
 __global__ void __launch_bounds__(CB_THREADS, 1)
     conv_band_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmO, const BandArgs a) {
+                     const __grid_constant__ CUtensorMap tmO,
+                     const __grid_constant__ CUtensorMap tmO2, const BandArgs a) {
   constexpr int RB = CGW * 2;                 // bytes per A row (one pixel's channel group)
-  constexpr int KSTEPS = CGW / 16;            // UMMA K steps per tap
+  constexpr int KSTEPS = CGW >= 16 ? CGW / 16 : 1;   // UMMA K steps per tap (CGW 8: per tap pair)
   constexpr int TAPS = R * S;
   constexpr int B_BLOCK = BN * 128;           // one 64-wide K block of weights
   extern __shared__ uint8_t smem_raw[];
@@ -91,7 +99,7 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
 
   const int warp = warp_index_uniform();
   const int lane = threadIdx.x & 31;
-  const int units = a.B * a.nbands * a.tiles_n;
+  const int units = a.B * a.nbands * a.nseg * a.tiles_n;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.a_stages; ++s) {
@@ -113,6 +121,7 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmO);
+    tma_prefetch_desc(&tmO2);
   }
   if (warp == 1) tmem_alloc(tmem_slot, a.tmem_cols);
   tc_fence_before();
@@ -134,13 +143,14 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int nt = u % a.tiles_n;
         const int rest = u / a.tiles_n;
-        const int band = rest % a.nbands;
-        const int img = rest / a.nbands;
+        const int seg = rest % a.nseg;
+        const int band = (rest / a.nseg) % a.nbands;
+        const int img = rest / a.nseg / a.nbands;
         for (int cg = 0; cg < a.CG; ++cg) {
           mbar_wait(&aempty[as], aph ^ 1);
           mbar_arrive_expect_tx(&afull[as], (uint32_t)a.a_box_bytes);
-          tma_load_4d(sA + as * a.a_stage_bytes, &tmA, &afull[as], cg * CGW, a.x0,
-                      band * a.bh + a.y0, img);
+          tma_load_4d(sA + as * a.a_stage_bytes, &tmA, &afull[as], cg * CGW,
+                      seg * a.seg_w + a.x0, band * a.bh + a.y0, img);
           if (++as == a.a_stages) {
             as = 0;
             aph ^= 1;
@@ -179,9 +189,11 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
     uint32_t aph = 0, bph = 0;
     int it = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
-      const int band = (u / a.tiles_n) % a.nbands;
+      const int seg = (u / a.tiles_n) % a.nseg;
+      const int band = (u / a.tiles_n / a.nseg) % a.nbands;
       const int vr = min(a.bh, a.H - band * a.bh);
-      const int mt_valid = ((vr - 1) * a.Wp + a.W - 1) / 128 + 1;
+      const int segw = seg < a.nseg - 1 ? a.seg_w : a.W - seg * a.seg_w;
+      const int mt_valid = ((vr - 1) * a.Wp + segw - 1) / 128 + 1;
       const int ab = it & 1;
       mbar_wait(&tempty[ab], ((it >> 1) & 1) ^ 1);
       tc_fence_after();
@@ -193,6 +205,22 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
         const uint64_t adesc0 = band_adesc<CGW>(smem_u32(sA + as * a.a_stage_bytes));
         for (int mt = 0; mt < mt_valid; ++mt) {
           const uint64_t adm = adesc0 + mt * MT_STEP;
+          if constexpr (CGW == 8) {
+            // tap pairs (r, 2q) + (r, 2q + 1): A start = pixel r * Wp + 2q
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+#pragma unroll
+              for (int qq = 0; qq < (S + 1) / 2; ++qq) {
+                const int kg = r * 32 + qq * 16;
+                const uint32_t boff =
+                    (uint32_t)((kg >> 6) * B_BLOCK + ((kg >> 4) & 3) * 32) >> 4;
+                if (elect_one())
+                  umma_bf16(dbase + mt * BN, adm + (uint32_t)(r * a.Wp + 2 * qq), bdesc0 + boff,
+                            idesc, (r | qq) != 0 ? 1u : 0u);
+              }
+            }
+            continue;
+          }
 #pragma unroll
           for (int t = 0; t < TAPS; ++t) {
 #pragma unroll
@@ -260,10 +288,13 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
       const int nt = u % a.tiles_n;
       const int rest = u / a.tiles_n;
-      const int band = rest % a.nbands;
-      const int img = rest / a.nbands;
+      const int seg = rest % a.nseg;
+      const int band = (rest / a.nseg) % a.nbands;
+      const int img = rest / a.nseg / a.nbands;
       const int vr = min(a.bh, a.H - band * a.bh);
-      const int mt_valid = ((vr - 1) * a.Wp + a.W - 1) / 128 + 1;
+      const int segw = seg < a.nseg - 1 ? a.seg_w : a.W - seg * a.seg_w;
+      const int mt_valid = ((vr - 1) * a.Wp + segw - 1) / 128 + 1;
+      const CUtensorMap* omap = seg == 0 ? &tmO : &tmO2;   // segment maps clip at their width
       const int n0 = nt * BN;
       const int ab = it & 1;
       if constexpr (BN == 64) {   // one 32-column chunk per warp: bias lives in registers
@@ -331,11 +362,11 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
             const uint8_t* src = obuf + (oi & 1) * 2048;
             if (a.Wp >= 32) {
               const int r = p0 / a.Wp;
-              if (r < vr) tma_store_4d(&tmO, src, n0 + c, p0 - r * a.Wp, band * a.bh + r, img);
+              if (r < vr) tma_store_4d(omap, src, n0 + c, p0 - r * a.Wp, band * a.bh + r, img);
             } else {
               for (int j = 0; j < 32 / a.Wp; ++j) {
                 const int r = p0 / a.Wp + j;
-                if (r < vr) tma_store_4d(&tmO, src + j * a.Wp * 64, n0 + c, 0, band * a.bh + r, img);
+                if (r < vr) tma_store_4d(omap, src + j * a.Wp * 64, n0 + c, 0, band * a.bh + r, img);
               }
             }
             bulk_commit();
@@ -370,9 +401,9 @@ int band_smem_bytes(const BandArgs& a, int bn) {
 static void band_geometry(BandArgs& a, int bh, int bn, int rb) {
   a.bh = bh;
   a.nbands = (a.H + bh - 1) / bh;
-  a.MT = ((bh - 1) * a.Wp + a.W - 1) / 128 + 1;
+  a.MT = ((bh - 1) * a.Wp + a.seg_w - 1) / 128 + 1;
   const int box_rows = (bh + a.R - 1) * a.Wp;
-  const int need_rows = a.MT * 128 + (a.R - 1) * a.Wp + (a.S - 1);
+  const int need_rows = a.MT * 128 + (a.R - 1) * a.Wp + (a.S - 1) + (rb == 16 ? 1 : 0);
   const int rows = ((box_rows > need_rows ? box_rows : need_rows) + 7) / 8 * 8;
   a.a_box_bytes = box_rows * rb;
   a.a_stage_bytes = (rows * rb + 1023) / 1024 * 1024;
@@ -399,7 +430,7 @@ bool band_config(BandArgs& a, int bn, int cgw, int mt_cap) {
     double computed = 0.0;
     for (int b = 0; b < bands; ++b) {
       const int vr = (a.H - b * bh) < bh ? (a.H - b * bh) : bh;
-      computed += (double)(((vr - 1) * a.Wp + a.W - 1) / 128 + 1) * 128;
+      computed += (double)(((vr - 1) * a.Wp + a.seg_w - 1) / 128 + 1) * 128 * a.nseg;
     }
     Cand c{bh, 0, 0, 0, (double)a.H * a.W / computed};
     BandArgs t = a;
@@ -409,6 +440,7 @@ bool band_config(BandArgs& a, int bn, int cgw, int mt_cap) {
     t.b_stages = 0;
     t.a_stages = 2;
     const bool res_ok = a.tiles_n == 1 && a.CG == 1 && bn == 64;   // instantiated resident kernels
+    (void)0;
     if (res_ok && band_smem_bytes(t, bn) <= CB_SMEM_MAX) {
       c.res = 1;
       c.ast = (a.CG > 1 && (t.a_stages = 3, band_smem_bytes(t, bn) <= CB_SMEM_MAX)) ? 3 : 2;
@@ -440,7 +472,8 @@ bool band_config(BandArgs& a, int bn, int cgw, int mt_cap) {
 
 template <int BN, int CGW, int R, int S, bool BRES, int ACT>
 static cudaError_t band_launch_t(const BandArgs& a, const CUtensorMap& ta, const CUtensorMap& tb,
-                                 const CUtensorMap& to, int num_sms, cudaStream_t st) {
+                                 const CUtensorMap& to, const CUtensorMap& to2, int num_sms,
+                                 cudaStream_t st) {
   auto kern = conv_band_kernel<BN, CGW, R, S, BRES, ACT>;
   static bool configured = false;
   if (!configured) {
@@ -449,29 +482,35 @@ static cudaError_t band_launch_t(const BandArgs& a, const CUtensorMap& ta, const
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int units = a.B * a.nbands * a.tiles_n;
+  const int units = a.B * a.nbands * a.nseg * a.tiles_n;
   const int grid = units < num_sms ? units : num_sms;
-  return launch_pdl(kern, dim3(grid), dim3(CB_THREADS), band_smem_bytes(a, BN), st, ta, tb, to, a);
+  return launch_pdl(kern, dim3(grid), dim3(CB_THREADS), band_smem_bytes(a, BN), st, ta, tb, to, to2,
+                    a);
 }
 
 template <int ACT>
 static cudaError_t band_dispatch(const BandArgs& a, int bn, int cgw, const CUtensorMap& ta,
-                                 const CUtensorMap& tb, const CUtensorMap& to, int num_sms,
-                                 cudaStream_t st) {
+                                 const CUtensorMap& tb, const CUtensorMap& to,
+                                 const CUtensorMap& to2, int num_sms, cudaStream_t st) {
   if (cgw == 16) {   // space-to-depth 7x7/2 stem: 4 x 4 taps, resident weights
     if (bn == 64 && a.R == 4 && a.S == 4 && a.b_resident && a.CG == 1)
-      return band_launch_t<64, 16, 4, 4, true, ACT>(a, ta, tb, to, num_sms, st);
+      return band_launch_t<64, 16, 4, 4, true, ACT>(a, ta, tb, to, to2, num_sms, st);
+    return cudaErrorInvalidValue;
+  }
+  if (cgw == 8) {    // 3x3 on an 8-channel padded image (VGG conv1_1)
+    if (bn == 64 && a.R == 3 && a.S == 3 && a.b_resident && a.CG == 1)
+      return band_launch_t<64, 8, 3, 3, true, ACT>(a, ta, tb, to, to2, num_sms, st);
     return cudaErrorInvalidValue;
   }
   if (a.R != 3 || a.S != 3) return cudaErrorInvalidValue;
   if (a.b_resident) {
-    if (bn == 64 && a.CG == 1) return band_launch_t<64, 64, 3, 3, true, ACT>(a, ta, tb, to, num_sms, st);
+    if (bn == 64 && a.CG == 1) return band_launch_t<64, 64, 3, 3, true, ACT>(a, ta, tb, to, to2, num_sms, st);
     return cudaErrorInvalidValue;
   }
   switch (bn) {
-    case 64: return band_launch_t<64, 64, 3, 3, false, ACT>(a, ta, tb, to, num_sms, st);
-    case 128: return band_launch_t<128, 64, 3, 3, false, ACT>(a, ta, tb, to, num_sms, st);
-    case 256: return band_launch_t<256, 64, 3, 3, false, ACT>(a, ta, tb, to, num_sms, st);
+    case 64: return band_launch_t<64, 64, 3, 3, false, ACT>(a, ta, tb, to, to2, num_sms, st);
+    case 128: return band_launch_t<128, 64, 3, 3, false, ACT>(a, ta, tb, to, to2, num_sms, st);
+    case 256: return band_launch_t<256, 64, 3, 3, false, ACT>(a, ta, tb, to, to2, num_sms, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -480,16 +519,17 @@ static cudaError_t band_dispatch(const BandArgs& a, int bn, int cgw, const CUten
 bool band_supported(const BandArgs& a, int bn, int cgw, int act) {
   if (act != ACT_NONE && act != ACT_RELU) return false;
   if (cgw == 16) return bn == 64 && a.R == 4 && a.S == 4 && a.b_resident && a.CG == 1;
+  if (cgw == 8) return bn == 64 && a.R == 3 && a.S == 3 && a.b_resident && a.CG == 1;
   if (a.R != 3 || a.S != 3) return false;
   if (a.b_resident) return bn == 64 && a.CG == 1;
   return bn == 64 || bn == 128 || bn == 256;
 }
 
 cudaError_t conv_band_launch(const BandArgs& a, int bn, int cgw, const CUtensorMap& ta,
-                             const CUtensorMap& tb, const CUtensorMap& to, int num_sms,
-                             cudaStream_t st) {
-  if (a.act == ACT_RELU) return band_dispatch<ACT_RELU>(a, bn, cgw, ta, tb, to, num_sms, st);
-  if (a.act == ACT_NONE) return band_dispatch<ACT_NONE>(a, bn, cgw, ta, tb, to, num_sms, st);
+                             const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& to2,
+                             int num_sms, cudaStream_t st) {
+  if (a.act == ACT_RELU) return band_dispatch<ACT_RELU>(a, bn, cgw, ta, tb, to, to2, num_sms, st);
+  if (a.act == ACT_NONE) return band_dispatch<ACT_NONE>(a, bn, cgw, ta, tb, to, to2, num_sms, st);
   return cudaErrorInvalidValue;
 }
 

@@ -57,6 +57,8 @@ struct BandArgs {
   int x0, y0;           // A box start offsets (-pad for zero-filled halos)
   int kblocks;          // Kpad / 64 (weight K blocks)
   int tiles_n;          // N / BN
+  int nseg, seg_w;      // column segments (rows wider than one band pitch): valid output
+                        // columns per segment (the last one takes the rest)
   // geometry chosen by band_config
   int bh, nbands, MT;
   int a_box_bytes, a_stage_bytes, a_stages, b_stages, b_resident, tmem_cols;
@@ -73,8 +75,8 @@ bool stem_pool_config(BandArgs& a);
 cudaError_t stem_pool_launch(const BandArgs& a, const CUtensorMap& ta, const CUtensorMap& tb,
                              int num_sms, cudaStream_t st);
 cudaError_t conv_band_launch(const BandArgs& a, int bn, int cgw, const CUtensorMap& ta,
-                             const CUtensorMap& tb, const CUtensorMap& to, int num_sms,
-                             cudaStream_t st);
+                             const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& to2,
+                             int num_sms, cudaStream_t st);
 
 // ---- chained 1x1 convs (chain_tc.cu): block tail conv -> next block's conv1 --
 struct ChainArgs {

@@ -205,6 +205,8 @@ struct Layer {
   int pool_op = -1;         // s2d stem: index of the 3x3/s2 max-pool fused into its epilogue
   int ds_op = -1;           // 1x1 conv: index of the projection shortcut folded into its K loop
   int chain_op = -1;        // block-tail 1x1 conv: next block's 1x1 conv computed in the same kernel
+  bool band8 = false;       // 3x3/s1 conv on an 8-channel padded image: conv_band CGW = 8,
+                            // weights [N][r][4][8] (paired taps, 4th tap zero)
   bool fused = false;       // max-pool executed inside its producer (no launch)
   int gmode = 0;            // see TcArgs::gmode
   int K = 0, kpad = 0, ldw = 0;
@@ -540,9 +542,25 @@ int upload_weights(b2_plan* pl, const uint8_t* data, const std::vector<WeightRec
             L.im2col = false;
             L.kpad = L.s2d_Rp * 64;
           }
+          L.band8 = conv && pl->use_band && C == 8 && R == 3 && S == 3 && L.p[10] == 1 &&
+                    L.p[11] == 1 && N % 64 == 0 && L.p[15] < 0 &&
+                    (L.p[14] == ACT_NONE || L.p[14] == ACT_RELU) && L.p[12] == L.p[4] &&
+                    L.p[13] == L.p[5] && !L.s2d;
+          if (L.band8) {
+            L.gather = false;
+            L.im2col = false;
+            L.kpad = 128;   // R * 32 = 96, padded to whole 64-wide weight blocks
+          }
           L.ldw = L.kpad;
           std::vector<float> h((size_t)N * L.kpad, 0.f);
-          if (L.s2d) {
+          if (L.band8) {
+            for (int n = 0; n < N; ++n)
+              for (int r = 0; r < 3; ++r)
+                for (int ss = 0; ss < 3; ++ss)
+                  for (int c = 0; c < 8; ++c)
+                    h[(size_t)n * L.kpad + r * 32 + ss * 8 + c] =
+                        w[(size_t)n * K + ((size_t)r * 3 + ss) * 8 + c];
+          } else if (L.s2d) {
             // W''[n][r'][s'][q], q = (dy*2+dx)*4 + c  <-  W[n][2r'+dy-1][2s'+dx-1][c]
             for (int n = 0; n < N; ++n)
               for (int rp = 0; rp < L.s2d_Rp; ++rp)
@@ -709,8 +727,8 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
         } else if (L.tc && S.band[li] && L.pool_op >= 0) {
           CK(stem_pool_launch(S.bargs[li], S.tmA[li], S.tmB[li], pl->num_sms, st));
         } else if (L.tc && S.band[li]) {
-          CK(conv_band_launch(S.bargs[li], S.bn[li], L.s2d ? 16 : 64, S.tmA[li], S.tmB[li],
-                              S.tmO[li], pl->num_sms, st));
+          CK(conv_band_launch(S.bargs[li], S.bn[li], L.s2d ? 16 : L.band8 ? 8 : 64, S.tmA[li], S.tmB[li],
+                              S.tmO[li], S.tmT[li], pl->num_sms, st));
         } else if (L.tc) {
           TcArgs a{};
           a.M = (int)M;
@@ -940,7 +958,7 @@ int band_pitch(int w) { return w <= 8 ? 8 : w <= 16 ? 16 : (w + 31) / 32 * 32; }
 int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
   Layer& L = pl->layers[li];
   const int* p = L.p;
-  if (!pl->use_band || L.kind != OP_CONV || p[15] >= 0) return 0;
+  if ((!pl->use_band && !L.band8) || L.kind != OP_CONV || p[15] >= 0) return 0;
   const int C = p[6], N = p[7], R = p[8], Sf = p[9], stride = p[10], pad = p[11];
   const int OH = p[12], OW = p[13];
   BandArgs a{};
@@ -952,6 +970,12 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
     a.R = a.S = L.s2d_Rp;
     a.CG = 1;
     a.x0 = a.y0 = 0;
+  } else if (L.band8) {
+    cgw = 8;
+    a.Wp = band_pitch(OW + 2);
+    a.R = a.S = 3;
+    a.CG = 1;
+    a.x0 = a.y0 = -1;
   } else {
     // N >= 256: the im2col GEMM's wide tiles already amortise A (measured:
     // band 62.8 / 108 us vs im2col 60.8 / 99.7 us on ResNet layer3 / layer4)
@@ -976,6 +1000,8 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
   a.out = reinterpret_cast<bf16*>(S.act[p[1]]);
   a.act = p[14];
   a.bias = L.bias ? L.bias : pl->zero_bias;
+  a.nseg = 1;
+  a.seg_w = OW;
   if (L.pool_op >= 0) {
     const int* q = pl->layers[L.pool_op].p;
     a.pout = reinterpret_cast<bf16*>(S.act[q[1]]);
@@ -984,7 +1010,13 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
     if (!stem_pool_config(a))
       return -fail(B2_ERR_UNSUPPORTED, "layer %zu: fused stem/max-pool geometry rejected", li);
   } else if (!band_config(a, bn, cgw) || !band_supported(a, bn, cgw, a.act)) {
-    return 0;
+    // rows too wide for one band pitch (VGG 224x224): split each row into two
+    // column segments of pitch 128 (126 valid columns + halo)
+    if (L.s2d || a.Wp <= 128 || OW > 2 * (128 - (Sf - 1))) return 0;
+    a.Wp = 128;
+    a.seg_w = 128 - (Sf - 1);
+    a.nseg = (OW + a.seg_w - 1) / a.seg_w;
+    if (!band_config(a, bn, cgw) || !band_supported(a, bn, cgw, a.act)) return 0;
   }
   if (L.pool_op < 0 && (long)a.B * a.nbands * a.tiles_n < pl->num_sms) {   // small batch: more, smaller units
     BandArgs t = a;
@@ -1003,20 +1035,28 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
   cuuint32_t es[4] = {1, 1, 1, 1};
   if (fn(&S.tmA[li], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, S.act[p[0]], dims, str, box, es,
          CU_TENSOR_MAP_INTERLEAVE_NONE,
-         cgw == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
+         cgw == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                   : cgw == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -fail(B2_ERR_CUDA, "layer %zu: band A tensor map rejected", li);
   if (!make_tmap_bf16(&S.tmB[li], L.w, (uint64_t)N, (uint64_t)L.kpad, (uint64_t)L.kpad * 2,
                       (uint32_t)bn))
     return -fail(B2_ERR_CUDA, "layer %zu: band B tensor map rejected", li);
-  // output NHWC [B, OH, OW, N]: 32-channel x 32-pixel boxes, 64 B swizzle
-  cuuint64_t odims[4] = {(cuuint64_t)N, (cuuint64_t)OW, (cuuint64_t)OH, (cuuint64_t)batch};
-  cuuint64_t ostr[3] = {(cuuint64_t)N * 2, (cuuint64_t)OW * N * 2, (cuuint64_t)OH * OW * N * 2};
-  cuuint32_t obox[4] = {32, 32, 1, 1};
-  if (fn(&S.tmO[li], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, S.act[p[1]], odims, ostr, obox, es,
-         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return -fail(B2_ERR_CUDA, "layer %zu: band output tensor map rejected", li);
+  // output NHWC [B, OH, OW, N]: 32-channel x 32-pixel boxes, 64 B swizzle;
+  // one map per column segment, each clipping at its own width
+  for (int sg = 0; sg < a.nseg && sg < 2; ++sg) {
+    const int w0 = sg * a.seg_w, wn = sg + 1 < a.nseg ? a.seg_w : OW - w0;
+    cuuint64_t odims[4] = {(cuuint64_t)N, (cuuint64_t)wn, (cuuint64_t)OH, (cuuint64_t)batch};
+    cuuint64_t ostr[3] = {(cuuint64_t)N * 2, (cuuint64_t)OW * N * 2, (cuuint64_t)OH * OW * N * 2};
+    cuuint32_t obox[4] = {32, 32, 1, 1};
+    CUtensorMap* m = sg == 0 ? &S.tmO[li] : &S.tmT[li];
+    if (fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, static_cast<bf16*>(S.act[p[1]]) + (size_t)w0 * N,
+           odims, ostr, obox, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return -fail(B2_ERR_CUDA, "layer %zu: band output tensor map rejected", li);
+  }
+  if (a.nseg > 2) return -fail(B2_ERR_UNSUPPORTED, "layer %zu: > 2 band segments", li);
+  if (a.nseg == 1) S.tmT[li] = S.tmO[li];
   S.bn[li] = bn;
   S.band[li] = 1;
   S.bargs[li] = a;
@@ -1071,6 +1111,8 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     int brc = plan_band(pl, S, li, batch);
     if (brc < 0) return -brc;
     if (brc == 1) continue;
+    if (L.band8)   // its weights are in the paired-tap layout only conv_band reads
+      return fail(B2_ERR_UNSUPPORTED, "layer %zu: 8-channel band conv geometry rejected", li);
     brc = plan_chain_state(pl, S, li, batch);
     if (brc < 0) return -brc;
     if (brc == 1) continue;

@@ -277,3 +277,10 @@ def test_chain(gpu_required, monkeypatch, H, C, Cm, N1, N2, shortcut, batch, cha
         pytest.skip("identity residual needs C == N1")
     monkeypatch.setenv("B2_CHAIN", chain)
     check(chain_plan(H, C, Cm, N1, N2, shortcut), batch)
+
+
+@pytest.mark.parametrize("H,batch", [(224, 1), (224, 3), (30, 5), (14, 40)])
+def test_band8_image_conv(gpu_required, H, batch):
+    """3x3/s1 conv on a 3-channel image padded to 8 (VGG conv1_1): the CGW = 8
+    band variant, paired taps per UMMA step over overlapping core matrices."""
+    check(conv_plan(H, H, 3, 64, 3, 1), batch)
