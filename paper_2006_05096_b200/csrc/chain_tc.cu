@@ -374,8 +374,9 @@ static int chain_smem(const ChainArgs& a) {
 
 bool chain_config(ChainArgs& a) {
   if (a.N1 % CH_BN != 0 || a.N2 % 64 != 0 || a.N2 < 64 || a.N2 > 256) return false;
-  for (a.b2_stages = 3; a.b2_stages >= 2; --a.b2_stages)
-    for (a.stages = 6; a.stages >= 2; --a.stages)
+  // the first GEMM's ring (A from HBM) needs the depth; two weight stages suffice
+  for (a.stages = 8; a.stages >= 2; --a.stages)
+    for (a.b2_stages = 3; a.b2_stages >= 2; --a.b2_stages)
       if (chain_smem(a) <= CH_SMEM_MAX) return true;
   return false;
 }

@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python -m pytest tests/test_gpu_conv.py -x -q -k "band8 or conv3x3" 2>&1 | tail -2
-timeout 600 python -m pytest tests/test_gpu.py -x -q -k "vgg" 2>&1 | tail -1
-timeout 60 python tools/conv_micro.py 256 224 224 3 64 3 1
-timeout 120 python tools/profile_ops.py vgg16 256 2>/dev/null | head -4
+for rep in 1 2; do for lib in ab/libb2_base.so paper_2006_05096_b200/libb2.so; do
+  B2_LIB=$PWD/$lib timeout 120 python bench.py --no-cpu --no-sweep --steps 50 | python3 -c "import json,sys; d=json.loads(sys.stdin.read()); print('$lib', d['ms_per_step'], d['value'], d['clocks']['sm_mhz'])"
+done; done
