@@ -264,7 +264,7 @@ struct b2_plan {
   bool force_simt = false;
   int launches = 0;
   int epi_mode = 0;          // B2_EPI_MODE: 0 TMA-store epilogue, 1 drain-only, 2 direct stores
-  int fold_max_k = 512;      // B2_FOLD_MAX_K: fold residuals into the MMA when K <= this
+  int fold_max_k = 1024;     // B2_FOLD_MAX_K: fold residuals into the MMA when K <= this
   bool use_im2col = true;    // B2_IM2COL=0 -> cp.async gather for C % 64 == 0 convs
   bool use_s2d = true;       // B2_S2D=0 -> stems on the cp.async gather path
   bool im2col8 = false;      // B2_IM2COL8=1 -> 8-channel-tap im2col TMA for C == 8 stems
