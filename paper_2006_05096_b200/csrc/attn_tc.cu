@@ -1,6 +1,6 @@
 // Fused self-attention on tcgen05 for seq = 128, head_dim = 64 (BERT-base).
 //
-// One CTA (4 warps) per (sample, head):
+// Per (sample, head) unit:
 //   1. TMA brings Q, K, V (each 128 x 64 bf16, 128B-swizzled) straight out of
 //      the fused QKV activation [B*S, 3*H*64].
 //   2. S = Q K^T on the tensor core (M=128 queries, N=128 keys, K=64) into TMEM.
@@ -16,7 +16,6 @@
 namespace b2 {
 
 constexpr int AT_S = 128, AT_D = 64;
-constexpr int AT_SMEM = 3 * 16384 + 2 * 16384 + 1024 + 64;
 
 // K-major A/B except B MN-major (bit 16) for the P*V product
 __host__ __device__ constexpr uint32_t idesc_bmn(int M, int N) {
@@ -33,25 +32,37 @@ B2_DEV uint64_t smem_desc_mn_sw128(uint32_t addr) {
   return d;
 }
 
-__global__ void __launch_bounds__(128, 2)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, bf16* __restrict__ out, int H) {
+// Persistent: one CTA per SM walks (sample, head) units; the next unit's
+// Q/K/V TMA load is issued into the other buffer before this unit's math, so
+// HBM latency overlaps compute.  8 warps: warps w and w + 4 share TMEM lane
+// quadrant w & 3 (query rows) and split the 128 keys (and the 64 output
+// columns) in halves; row max / sum are combined through shared memory.
+constexpr int AT_WARPS = 8;
+constexpr int AT_QKV = 3 * 16384;
+constexpr int AT_SMEM = 2 * AT_QKV + 2 * 16384 + 4 * 128 * 4 + 1024 + 64;
+
+B2_DEV void at_bar() { asm volatile("bar.sync 1, %0;" ::"n"(AT_WARPS * 32) : "memory"); }
+
+__global__ void __launch_bounds__(AT_WARPS * 32, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, bf16* __restrict__ out, int H,
+                   int units) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = smem + 16384;
-  uint8_t* sV = smem + 32768;
-  uint8_t* sP = smem + 49152;   // two 16 KB atoms: keys 0-63, 64-127
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 81920);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+  uint8_t* sQKV = smem;                       // 2 buffers x (Q | K | V), 16 KB each
+  uint8_t* sP = smem + 2 * AT_QKV;            // two 16 KB atoms: keys 0-63, 64-127
+  float* red = reinterpret_cast<float*>(sP + 2 * 16384);   // [2 stats][2 halves][128 rows]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 4 * 128);   // load[2], mma
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3);
 
   const int warp = warp_index_uniform(), lane = threadIdx.x & 31;
-  const int b = blockIdx.x / H, h = blockIdx.x % H;
-  const int row0 = b * AT_S;
+  const int q = warp & 3, hh = warp >> 2;
+  const int row = q * 32 + lane;
 
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(tslot, 256);
@@ -62,96 +73,115 @@ __global__ void __launch_bounds__(128, 2)
   pdl_wait();
   pdl_launch_dependents();
 
-  if (warp == 0) {   // converged warp, elected lane issues (common.cuh)
-    if (elect_one()) {
-      mbar_arrive_expect_tx(&bars[0], 3 * 16384);
-      tma_load_2d(sQ, &tmQKV, &bars[0], h * AT_D, row0);
-      tma_load_2d(sK, &tmQKV, &bars[0], (H + h) * AT_D, row0);
-      tma_load_2d(sV, &tmQKV, &bars[0], (2 * H + h) * AT_D, row0);
-    }
-    __syncwarp();
-    mbar_wait(&bars[0], 0);
-    tc_fence_after();
-    const uint64_t dq = smem_desc_sw128(smem_u32(sQ));
-    const uint64_t dk = smem_desc_sw128(smem_u32(sK));
-#pragma unroll
-    for (int k = 0; k < AT_D / 16; ++k)
-      if (elect_one()) umma_bf16(tbase, dq + 2 * k, dk + 2 * k, make_idesc(128, 128, 1u), k ? 1u : 0u);
-    if (elect_one()) umma_commit(&bars[1]);
-  }
-  mbar_wait(&bars[1], 0);
-  tc_fence_after();
+  auto issue_load = [&](int u, int buf) {
+    const int b = u / H, h = u - (u / H) * H;
+    uint8_t* d = sQKV + buf * AT_QKV;
+    mbar_arrive_expect_tx(&bars[buf], AT_QKV);
+    tma_load_2d(d, &tmQKV, &bars[buf], h * AT_D, b * AT_S);
+    tma_load_2d(d + 16384, &tmQKV, &bars[buf], (H + h) * AT_D, b * AT_S);
+    tma_load_2d(d + 32768, &tmQKV, &bars[buf], (2 * H + h) * AT_D, b * AT_S);
+  };
+  if (threadIdx.x == 0 && (int)blockIdx.x < units) issue_load(blockIdx.x, 0);
 
-  // ---- softmax over this thread's query row (TMEM lane = row)
-  const int row = warp * 32 + lane;
-  const uint32_t trow = tbase + (uint32_t(warp * 32) << 16);
-  float s[128];
-  {
-    uint32_t r[32];
+  const float scl = 0.125f * 1.4426950408889634f;   // 1/sqrt(64) * log2(e)
+  uint32_t mph = 0;
+  int it = 0;
+  for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+    const int buf = it & 1;
+    // prefetch the next unit into the other buffer (its previous user is done)
+    if (threadIdx.x == 0 && u + (int)gridDim.x < units) issue_load(u + gridDim.x, buf ^ 1);
+    mbar_wait(&bars[buf], (it >> 1) & 1);
+    tc_fence_after();
+    uint8_t* sQ = sQKV + buf * AT_QKV;
+    if (warp == 0) {   // S = Q K^T (M=128 queries, N=128 keys, K=64)
+      const uint64_t dq = smem_desc_sw128(smem_u32(sQ));
+      const uint64_t dk = smem_desc_sw128(smem_u32(sQ + 16384));
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      tmem_ld_32x32b_x32(trow + c * 32, r);
+      for (int k = 0; k < AT_D / 16; ++k)
+        if (elect_one()) umma_bf16(tbase, dq + 2 * k, dk + 2 * k, make_idesc(128, 128, 1u), k ? 1u : 0u);
+      if (elect_one()) umma_commit(&bars[2]);
+    }
+    mbar_wait(&bars[2], mph);
+    mph ^= 1;
+    tc_fence_after();
+
+    // ---- softmax: this thread's row, key half hh (64 scores)
+    const uint32_t trow = tbase + (uint32_t(q * 32) << 16) + hh * 64;
+    float sv[64];
+    {
+      uint32_t r0[32], r1[32];
+      tmem_ld_32x32b_x32(trow, r0);
+      tmem_ld_32x32b_x32(trow + 32, r1);
       tmem_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 32; ++j) s[c * 32 + j] = __uint_as_float(r[j]);
+      for (int j = 0; j < 32; ++j) {
+        sv[j] = __uint_as_float(r0[j]);
+        sv[32 + j] = __uint_as_float(r1[j]);
+      }
     }
-  }
-  const float scl = 0.125f * 1.4426950408889634f;   // 1/sqrt(64) * log2(e)
-  float mx = s[0];
+    float mx = sv[0];
 #pragma unroll
-  for (int j = 1; j < 128; ++j) mx = fmaxf(mx, s[j]);
-  const float off = mx * scl;
-  float sum = 0.f;
+    for (int j = 1; j < 64; ++j) mx = fmaxf(mx, sv[j]);
+    red[hh * 128 + row] = mx;
+    at_bar();
+    mx = fmaxf(red[row], red[128 + row]);
+    const float off = mx * scl;
+    float sum = 0.f;
 #pragma unroll
-  for (int j = 0; j < 128; ++j) {
-    s[j] = exp2f(fmaf(s[j], scl, -off));
-    sum += s[j];
-  }
+    for (int j = 0; j < 64; ++j) {
+      sv[j] = exp2f(fmaf(sv[j], scl, -off));
+      sum += sv[j];
+    }
+    red[256 + hh * 128 + row] = sum;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {   // 8 keys per 16-byte chunk
-    uint4 u;
-    u.x = pack_bf16x2(s[8 * j + 0], s[8 * j + 1]);
-    u.y = pack_bf16x2(s[8 * j + 2], s[8 * j + 3]);
-    u.z = pack_bf16x2(s[8 * j + 4], s[8 * j + 5]);
-    u.w = pack_bf16x2(s[8 * j + 6], s[8 * j + 7]);
-    uint8_t* dst = sP + (j >> 3) * 16384 + row * 128 + ((((j & 7) ^ (row & 7))) << 4);
-    *reinterpret_cast<uint4*>(dst) = u;
-  }
-  fence_proxy_async_smem();
-  tc_fence_before();
-  __syncthreads();
+    for (int j = 0; j < 8; ++j) {   // 8 keys per 16-byte chunk of atom hh
+      uint4 w;
+      w.x = pack_bf16x2(sv[8 * j + 0], sv[8 * j + 1]);
+      w.y = pack_bf16x2(sv[8 * j + 2], sv[8 * j + 3]);
+      w.z = pack_bf16x2(sv[8 * j + 4], sv[8 * j + 5]);
+      w.w = pack_bf16x2(sv[8 * j + 6], sv[8 * j + 7]);
+      *reinterpret_cast<uint4*>(sP + hh * 16384 + row * 128 + ((j ^ (row & 7)) << 4)) = w;
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    at_bar();
+    sum = red[256 + row] + red[384 + row];
 
-  if (warp == 0) {
+    if (warp == 0) {   // O = P V (M=128, N=64, K=128; V MN-major as stored)
+      tc_fence_after();
+      const uint32_t pbase = smem_u32(sP);
+      const uint32_t vbase = smem_u32(sQ + 32768);
+#pragma unroll
+      for (int k = 0; k < AT_S / 16; ++k) {
+        const uint64_t da = smem_desc_sw128(pbase + (k >> 2) * 16384 + (k & 3) * 32);
+        const uint64_t dv = smem_desc_mn_sw128(vbase + k * 16 * 128);
+        if (elect_one()) umma_bf16(tbase + 128, da, dv, idesc_bmn(128, 64), k ? 1u : 0u);
+      }
+      if (elect_one()) umma_commit(&bars[2]);
+    }
+    mbar_wait(&bars[2], mph);
+    mph ^= 1;
     tc_fence_after();
-    const uint32_t pbase = smem_u32(sP);
-    const uint32_t vbase = smem_u32(sV);
-#pragma unroll
-    for (int k = 0; k < AT_S / 16; ++k) {
-      const uint64_t da = smem_desc_sw128(pbase + (k >> 2) * 16384 + (k & 3) * 32);
-      const uint64_t dv = smem_desc_mn_sw128(vbase + k * 16 * 128);
-      if (elect_one()) umma_bf16(tbase + 128, da, dv, idesc_bmn(128, 64), k ? 1u : 0u);
-    }
-    if (elect_one()) umma_commit(&bars[1]);
-  }
-  mbar_wait(&bars[1], 1);
-  tc_fence_after();
 
-  const float inv = 1.f / sum;
-  uint4* orow = reinterpret_cast<uint4*>(out + (size_t)(row0 + row) * (H * AT_D) + h * AT_D);
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
+    // ---- context: this thread's row, output columns hh*32 .. +32
+    const int b = u / H, h = u - (u / H) * H;
+    const float inv = 1.f / sum;
     uint32_t r[32];
-    tmem_ld_32x32b_x32(trow + 128 + c * 32, r);
+    tmem_ld_32x32b_x32(tbase + (uint32_t(q * 32) << 16) + 128 + hh * 32, r);
     tmem_wait_ld();
+    uint4* orow = reinterpret_cast<uint4*>(out + (size_t)(b * AT_S + row) * (H * AT_D) + h * AT_D +
+                                           hh * 32);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint4 u;
-      u.x = pack_bf16x2(__uint_as_float(r[8 * q + 0]) * inv, __uint_as_float(r[8 * q + 1]) * inv);
-      u.y = pack_bf16x2(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv);
-      u.z = pack_bf16x2(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv);
-      u.w = pack_bf16x2(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv);
-      orow[c * 4 + q] = u;
+    for (int j = 0; j < 4; ++j) {
+      uint4 w;
+      w.x = pack_bf16x2(__uint_as_float(r[8 * j + 0]) * inv, __uint_as_float(r[8 * j + 1]) * inv);
+      w.y = pack_bf16x2(__uint_as_float(r[8 * j + 2]) * inv, __uint_as_float(r[8 * j + 3]) * inv);
+      w.z = pack_bf16x2(__uint_as_float(r[8 * j + 4]) * inv, __uint_as_float(r[8 * j + 5]) * inv);
+      w.w = pack_bf16x2(__uint_as_float(r[8 * j + 6]) * inv, __uint_as_float(r[8 * j + 7]) * inv);
+      orow[j] = w;
     }
+    tc_fence_before();
+    at_bar();   // S / O TMEM, P smem and the red[] stats are reused by the next unit
   }
   tc_fence_before();
   __syncthreads();
@@ -169,7 +199,12 @@ cudaError_t attention_tc(const CUtensorMap& tm_qkv, bf16* out, int B, int H, cud
     if (e != cudaSuccess) return e;
     cfg = true;
   }
-  return launch_pdl(attn_tc_kernel, dim3(B * H), dim3(128), AT_SMEM, st, tm_qkv, out, H);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int units = B * H;
+  return launch_pdl(attn_tc_kernel, dim3(units < sms ? units : sms), dim3(AT_WARPS * 32), AT_SMEM,
+                    st, tm_qkv, out, H, units);
 }
 
 }  // namespace b2
