@@ -64,6 +64,11 @@ B2_DEV void add_bf16x8(float* v, const uint4& u) {
 
 // TMA-store epilogue of one warp, specialised on the activation so the
 // per-element math is branch-free.
+B2_DEV void split_range(int s, int nsplit, int KT, int& kb0, int& kb1) {
+  kb0 = (int)((long)s * KT / nsplit);
+  kb1 = (int)((long)(s + 1) * KT / nsplit);
+}
+
 // M tile of linear tile index t.  Consecutive layers alternate the M
 // direction (a.reverse): the next kernel then starts on the rows its producer
 // wrote last, which are still in L2.
@@ -214,6 +219,12 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
   const int warp = warp_index_uniform();
   const int lane = threadIdx.x & 31;
   const int ntiles = a.tiles_m * a.tiles_n;
+  // split-K (small batches): unit u = split (u / ntiles) of tile (u % ntiles);
+  // each split stores its fp32 partial into its own workspace slice and
+  // splitk_finalize sums the slices in order (deterministic) and applies
+  // bias, residual, activation, bf16
+  const int nunits = ntiles * a.nsplit;
+  const int KT = a.kblocks + a.res_kblocks;
 
   __shared__ unsigned long long ts[8];    // B2_GEMM_TS phase timestamps (globaltimer, ns)
   auto stamp = [&](int i) {
@@ -259,7 +270,10 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       const int cpb = a.C >> 6;   // im2col: 64-channel K blocks per filter tap
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int t = u % ntiles;
+        int kb0, kb1;
+        split_range(u / ntiles, a.nsplit, KT, kb0, kb1);
         const int m0 = mtile_of(a, t) * TC_BM;
         const int n0 = (t % a.tiles_n) * BN;
         int iw0 = 0, ih0 = 0, img = 0;
@@ -270,7 +284,7 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
           ih0 = oh * a.stride - a.pad;
           iw0 = (rem - oh * a.OW) * a.stride - a.pad;
         }
-        for (int kb = 0; kb < a.kblocks + a.res_kblocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (kb >= a.kblocks) {
             const int j = kb - a.kblocks;
@@ -345,13 +359,15 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+        int kb0, kb1;
+        split_range(u / ntiles, a.nsplit, KT, kb0, kb1);
         const int as = it & 1;
         const uint32_t aph = (it >> 1) & 1;
         mbar_wait(&tempty[as], aph ^ 1);
         tc_fence_after();
         const uint32_t dt = tmem_base + as * BN;
-        for (int kb = 0; kb < a.kblocks + a.res_kblocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (it == 0 && kb == 0 && lane == 0) stamp(2);
@@ -363,7 +379,8 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
           const uint64_t bd = smem_desc_sw128(smem_u32(sB + stage * Cfg::B_BYTES));
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k)
-            if (elect_one()) umma_bf16(dt, ad + astep * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+            if (elect_one())
+              umma_bf16(dt, ad + astep * k, bd + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           if (elect_one()) umma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
@@ -395,6 +412,34 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
           acc ^= r[0] ^ r[31];
         }
         if (acc == 0x7f7f7f7fu) a.out[0] = __float2bfloat16_rn(0.f);   // keep the loads alive
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[as]);
+      }
+    } else if (a.nsplit > 1) {
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+        const int t = u % ntiles;
+        const int as = it & 1;
+        mbar_wait(&tfull[as], (it >> 1) & 1);
+        tc_fence_after();
+        const int row = mtile_of(a, t) * TC_BM + lg * 32 + lane;
+        const int n0 = (t % a.tiles_n) * BN;
+        const uint32_t taddr = tmem_base + (uint32_t(lg * 32) << 16) + as * BN;
+#pragma unroll 1
+        for (int c = eh * 32; c < BN; c += 64) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + c, r);
+          tmem_wait_ld();
+          if (row < a.M && n0 + c < a.N) {   // this split's slice: deterministic order
+            float4* dst = reinterpret_cast<float4*>(
+                a.ws + ((size_t)(u / ntiles) * a.M + row) * a.N + n0 + c);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)   // ragged last N tile: columns < N only (N % 8 == 0)
+              if (n0 + c + 4 * q < a.N)
+                dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                     __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+          }
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[as]);
@@ -782,8 +827,8 @@ static cudaError_t launch_bn(TcArgs a, const CUtensorMap& ta, const CUtensorMap&
     configured = true;
   }
   if (a.stages <= 0 || a.stages > Cfg::MAX_STAGES) a.stages = Cfg::MAX_STAGES;
-  const int tiles = a.tiles_m * a.tiles_n;
-  const int grid = tiles < num_sms ? tiles : num_sms;
+  const int units = a.tiles_m * a.tiles_n * a.nsplit;
+  const int grid = units < num_sms ? units : num_sms;
   return launch_pdl(kern, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, ta, tb, to, tr, ti, a);
 }
 
@@ -831,6 +876,17 @@ int tc2_pick_bn(long M, int N, int num_sms) {
     }
   }
   return best;
+}
+
+// Split-K factor for small batches: when the tiles cannot fill half the SMs
+// and the K loop is long, spread each tile's K over up to 16 CTAs (>= 4 K
+// blocks each).  Large batches keep nsplit = 1.
+int tc_pick_split(long tiles, int kt, int num_sms) {
+  if (tiles * 2 > num_sms || kt < 8) return 1;
+  int sp = (int)(num_sms / tiles);
+  if (sp > kt / 4) sp = kt / 4;
+  if (sp > 16) sp = 16;
+  return sp < 2 ? 1 : sp;
 }
 
 int tc_pick_bn(long M, int N, int num_sms) {

@@ -499,6 +499,64 @@ cudaError_t maxpool(const T* x, T* y, int B, int H, int W, int C, int k, int str
   return cudaGetLastError();
 }
 
+// Split-K epilogue: out = act(sum_s ws[s] + bias + res) in bf16, slices
+// summed in split order (bit-reproducible), 8 outputs per thread.
+template <int ACT>
+__global__ void splitk_finalize_kernel(const float* __restrict__ ws, int nsplit,
+                                       const float* __restrict__ bias,
+                                       const bf16* __restrict__ res, bf16* __restrict__ out,
+                                       long M, int N) {
+  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (i >= M * N) return;
+  const int n = (int)(i % N);
+  float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int sp = 0; sp < nsplit; ++sp) {
+    const float4* w4 = reinterpret_cast<const float4*>(ws + (size_t)sp * M * N + i);
+    const float4 a = __ldcg(w4), b = __ldcg(w4 + 1);
+    v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+    v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+  }
+  if (bias) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] += __ldg(bias + n + e);
+  }
+  if (res) {
+    const uint4 r = __ldg(reinterpret_cast<const uint4*>(res + i));
+    const uint32_t rw[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const float2 f = unpack_bf16x2(rw[h]);
+      v[2 * h] += f.x;
+      v[2 * h + 1] += f.y;
+    }
+  }
+  uint4 o;
+  o.x = pack_bf16x2(act_t<ACT>(v[0]), act_t<ACT>(v[1]));
+  o.y = pack_bf16x2(act_t<ACT>(v[2]), act_t<ACT>(v[3]));
+  o.z = pack_bf16x2(act_t<ACT>(v[4]), act_t<ACT>(v[5]));
+  o.w = pack_bf16x2(act_t<ACT>(v[6]), act_t<ACT>(v[7]));
+  *reinterpret_cast<uint4*>(out + i) = o;
+}
+
+cudaError_t splitk_finalize(const float* ws, int nsplit, const float* bias, const bf16* res,
+                            bf16* out, long M, int N, int act, cudaStream_t st) {
+  if (N % 8 != 0) return cudaErrorInvalidValue;
+  const long th = M * N / 8;
+  switch (act) {
+#define B2_SKF(A)                                                                              \
+  case A:                                                                                      \
+    splitk_finalize_kernel<A><<<nblk(th, 256), 256, 0, st>>>(ws, nsplit, bias, res, out, M, N); \
+    return cudaGetLastError();
+    B2_SKF(ACT_NONE)
+    B2_SKF(ACT_RELU)
+    B2_SKF(ACT_RELU6)
+    B2_SKF(ACT_GELU)
+    B2_SKF(ACT_TANH)
+#undef B2_SKF
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <typename T>
 __global__ void avgpool_kernel(const T* __restrict__ x, T* __restrict__ y, int B, int HW, int C) {
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;

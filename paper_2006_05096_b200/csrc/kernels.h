@@ -41,6 +41,8 @@ struct TcArgs {
                         // 2 = one 8-channel filter tap per 2 KB box (C == 8 stems), 8 taps
                         //     per K block in the non-swizzled K-major layout
   int reverse;          // walk M tiles last-to-first (L2 reuse across layers)
+  int nsplit;           // split-K factor (1 = none): partials red.add'ed into ws
+  float* ws;            // split-K fp32 partials [nsplit][M][N]
   int fold_kind;        // extra K blocks: 0 residual x identity; 1 shortcut x (stride 1, 2D)
                         // against its weights; 2 strided shortcut x (im2col TMA)
   int ds_H, ds_W;       // fold_kind 2: shortcut input geometry (uses OW, OHW, stride too)
@@ -97,6 +99,9 @@ cudaError_t chain_launch(const ChainArgs& a, const CUtensorMap& tA, const CUtens
                          cudaStream_t st);
 
 int tc_pick_bn(long M, int N, int num_sms);
+int tc_pick_split(long tiles, int kt, int num_sms);
+cudaError_t splitk_finalize(const float* ws, int nsplit, const float* bias, const bf16* res,
+                            bf16* out, long M, int N, int act, cudaStream_t st);
 int tc2_pick_bn(long M, int N, int num_sms);
 cudaError_t tc_gemm2_launch(const TcArgs& a, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                             const CUtensorMap& to, const CUtensorMap& tr, const CUtensorMap& ti,

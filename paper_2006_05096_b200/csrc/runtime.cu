@@ -228,6 +228,8 @@ struct BatchState {
   std::vector<char> band;          // per layer: banded implicit-GEMM conv (conv_band.cu)
   std::vector<char> pair;          // per layer: CTA-pair GEMM (tc_gemm2_kernel)
   std::vector<char> chain;         // per layer: chained with the next conv1 (chain_tc.cu)
+  std::vector<int> split;          // per layer: split-K factor (small batches)
+  float* ws = nullptr;             // split-K fp32 partial slices (shared by the layers)
   std::vector<ChainArgs> cargs;
   std::vector<CUtensorMap> tmB2, tmT;   // chain: second weights, second output
   std::vector<BandArgs> bargs;     // per layer (band): geometry chosen by band_config
@@ -276,6 +278,7 @@ struct b2_plan {
   bool use_pool_fusion = true;   // B2_POOL_FUSION=0 -> stem and max-pool as two kernels
   bool use_ds_fold = true;       // B2_DS_FOLD=0 -> projection shortcuts as their own kernels
   bool alt_order = true;         // B2_ALT_ORDER=0 -> every GEMM walks M tiles forward
+  bool use_split = true;         // B2_SPLIT=0 -> no split-K at small batch
   bool use_chain = true;         // B2_CHAIN=0 -> block-tail and next conv1 as two GEMMs
   int band_max_n = 128;      // B2_BAND_MAX_N: widest conv (output channels) sent to conv_band
   void* identity = nullptr;  // bf16 I[256][256]
@@ -731,6 +734,7 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
                               S.tmO[li], S.tmT[li], pl->num_sms, st));
         } else if (L.tc) {
           TcArgs a{};
+          a.nsplit = 1;
           a.M = (int)M;
           a.N = N;
           a.kblocks = L.kpad / 64;
@@ -790,6 +794,17 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
             CK(tc_gemm2_launch(a, bn, S.tmA[li], S.tmB[li], S.tmO[li],
                                S.fold[li] ? S.tmR[li] : S.tmO[li],
                                S.fold[li] ? S.tmI[li] : S.tmO[li], pl->num_sms, st));
+          } else if (S.split[li] > 1) {
+            a.nsplit = S.split[li];
+            a.ws = S.ws;
+            a.res = nullptr;
+            a.res_kblocks = 0;
+            CK(tc_gemm_launch(a, bn, false, S.tmA[li], S.tmB[li], S.tmO[li], S.tmO[li], S.tmO[li],
+                              pl->num_sms, st));
+            CK(splitk_finalize(S.ws, a.nsplit, L.bias,
+                               res_t >= 0 ? reinterpret_cast<const bf16*>(S.act[res_t]) : nullptr,
+                               reinterpret_cast<bf16*>(out), M, N, act, st));
+            ++launches;
           } else {
             CK(tc_gemm_launch(a, bn, L.gather, L.gather ? S.tmB[li] : S.tmA[li], S.tmB[li],
                               S.tmO[li], S.fold[li] ? S.tmR[li] : S.tmO[li],
@@ -1100,6 +1115,8 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
   S.band.assign(pl->layers.size(), 0);
   S.pair.assign(pl->layers.size(), 0);
   S.chain.assign(pl->layers.size(), 0);
+  S.split.assign(pl->layers.size(), 1);
+  size_t ws_elems = 0;
   S.cargs.resize(pl->layers.size());
   S.tmB2.resize(pl->layers.size());
   S.tmT.resize(pl->layers.size());
@@ -1142,6 +1159,15 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     if (pl->force_bn && !pair_ok && N % pl->force_bn == 0) bn = pl->force_bn;   // B2_FORCE_BN (tuning aid)
     S.bn[li] = bn;
     S.pair[li] = pair_ok;
+    if (!pair_ok && !L.gather && !L.s2d && L.ds_op < 0 && bn >= 32 && N % 8 == 0 &&
+        pl->use_split && pl->epi_mode == 0) {
+      const long tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
+      const int sp = tc_pick_split(tiles, L.kpad / 64, pl->num_sms);
+      if (sp > 1) {
+        S.split[li] = sp;
+        ws_elems = std::max(ws_elems, (size_t)sp * M * N);
+      }
+    }
     const uint32_t bbox = pair_ok ? bn / 2 : bn;
     if (!make_tmap_bf16(&S.tmB[li], L.w, (uint64_t)N, (uint64_t)L.kpad, (uint64_t)L.kpad * 2,
                         bbox))
@@ -1192,7 +1218,8 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
                                  (uint64_t)D.kpad * 2, bbox))
         return fail(B2_ERR_CUDA, "layer %zu: folded shortcut tensor maps rejected", li);
       S.fold[li] = q[10] == 1 ? 2 : 3;
-    } else if (res_t >= 0 && bn >= 64 && N % 8 == 0 && L.K <= pl->fold_max_k && pl->identity) {
+    } else if (res_t >= 0 && bn >= 64 && N % 8 == 0 && L.K <= pl->fold_max_k && pl->identity &&
+               S.split[li] == 1) {   // split-K adds the residual in its finalize pass
       if (!make_tmap_bf16(&S.tmR[li], S.act[res_t], (uint64_t)M, (uint64_t)N, (uint64_t)N * 2,
                           128) ||
           !make_tmap_bf16(&S.tmI[li], pl->identity, 256, 256, 512, bbox))
@@ -1210,6 +1237,10 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
       if (!make_tmap_bf16(&S.tmA[li], S.act[p[0]], (uint64_t)M, (uint64_t)K, (uint64_t)ld * 2, 128))
         return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeTiled(A) failed", li);
     }
+  }
+  if (ws_elems) {
+    CK(cudaMalloc(&S.ws, ws_elems * sizeof(float) + 256));
+    CK(cudaMemset(S.ws, 0, ws_elems * sizeof(float) + 256));
   }
   auto res = pl->states.emplace(batch, std::move(S));
   *out = &res.first->second;
@@ -1319,6 +1350,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* pf = getenv("B2_POOL_FUSION")) pl->use_pool_fusion = pf[0] != '0';
   if (const char* df = getenv("B2_DS_FOLD")) pl->use_ds_fold = df[0] != '0';
   if (const char* ao = getenv("B2_ALT_ORDER")) pl->alt_order = ao[0] != '0';
+  if (const char* sk = getenv("B2_SPLIT")) pl->use_split = sk[0] != '0';
   if (const char* cz = getenv("B2_CHAIN")) pl->use_chain = cz[0] != '0';
   if (const char* bm = getenv("B2_BAND_MAX_N")) pl->band_max_n = atoi(bm);
   cudaGetDevice(&pl->device);
@@ -1648,6 +1680,7 @@ void b2_plan_destroy(b2_plan* pl) {
     if (S.h_in) cudaFreeHost(S.h_in);
     if (S.h_out) cudaFreeHost(S.h_out);
     if (S.graph2) cudaGraphExecDestroy(S.graph2);
+    if (S.ws) cudaFree(S.ws);
     if (S.d_in2) cudaFree(S.d_in2);
     if (S.d_out2) cudaFree(S.d_out2);
     if (S.h_out2) cudaFreeHost(S.h_out2);

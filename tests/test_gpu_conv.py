@@ -284,3 +284,24 @@ def test_band8_image_conv(gpu_required, H, batch):
     """3x3/s1 conv on a 3-channel image padded to 8 (VGG conv1_1): the CGW = 8
     band variant, paired taps per UMMA step over overlapping core matrices."""
     check(conv_plan(H, H, 3, 64, 3, 1), batch)
+
+
+@pytest.mark.parametrize("M,K,N,res", [
+    (300, 2048, 512, False),   # 6 tiles, 32 K blocks: split 8
+    (200, 1024, 512, True),    # split + residual added in the finalize pass
+    (64, 4096, 1024, True),
+    (2, 2048, 1000, False),    # ResNet fc at batch 2: ragged last N tile (1000 = 3 x 256 + 232)
+])
+@pytest.mark.parametrize("split", ["1", "0"])
+def test_split_k(gpu_required, monkeypatch, M, K, N, res, split):
+    """Small-batch split-K (partials red.add'ed into an fp32 workspace, then a
+    finalize pass adds bias / residual / activation) against the oracle."""
+    monkeypatch.setenv("B2_SPLIT", split)
+    monkeypatch.setenv("B2_PAIR", "0")
+    check(linear_plan(K, N, res), M)
+
+
+@pytest.mark.parametrize("batch", [1, 4])
+def test_split_k_conv(gpu_required, batch):
+    """layer4 3x3 (K = 4608) at small batch: im2col A under split-K."""
+    check(conv_plan(7, 7, 512, 512, 3, 1), batch)
