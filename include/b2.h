@@ -109,7 +109,10 @@ B2_API int b2_profile_ops(b2_plan* plan, int batch, int iters, float* op_ms, int
 
 /* Copy activation tensor `tensor` (as stored: bf16/fp32, or int32 ids) of the
  * last forward run at `batch` into host memory (verification hook: lets the
- * parity tests check every op against the oracle on the kernel's own inputs). */
+ * parity tests check every op against the oracle on the kernel's own inputs).
+ * Returns B2_ERR_FUSED for intermediates the executor never materialises
+ * (the stem output under the fused stem/max-pool, a ResNet projection
+ * shortcut folded into its block's last conv). */
 B2_API int b2_read_tensor(b2_plan* plan, int batch, int tensor, void* host_out, size_t bytes);
 
 B2_API void b2_plan_destroy(b2_plan* plan);
