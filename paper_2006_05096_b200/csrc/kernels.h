@@ -99,6 +99,8 @@ cudaError_t chain_launch(const ChainArgs& a, const CUtensorMap& tA, const CUtens
                          cudaStream_t st);
 
 int tc_pick_bn(long M, int N, int num_sms);
+cudaError_t tf32_gemm_launch(const TcArgs& a, const CUtensorMap& ta, const CUtensorMap& tbh,
+                             const CUtensorMap& tbl, int num_sms, cudaStream_t st);
 int tc_pick_split(long tiles, int kt, int num_sms);
 cudaError_t splitk_finalize(const float* ws, int nsplit, const float* bias, const bf16* res,
                             bf16* out, long M, int N, int act, cudaStream_t st);

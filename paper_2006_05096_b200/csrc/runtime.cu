@@ -140,6 +140,21 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t co
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// fp32 matrix [rows, cols] with row pitch in bytes; box = 32 cols (128 B) x
+// box_rows, 128-byte swizzle (the 3xTF32 GEMM's K-major operand layout)
+bool make_tmap_f32(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
+                   uint64_t row_bytes, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const int*, const int*,
                                    cuuint32_t, cuuint32_t, const cuuint32_t*,
@@ -162,23 +177,27 @@ EncodeIm2colFn encode_im2col_fn() {
 // NHWC bf16 activation [N, H, W, C] for implicit-GEMM conv A tiles: 128 output
 // pixels x 64 channels per load, filter offsets supplied per load
 bool make_tmap_im2col(CUtensorMap* m, const void* base, int N, int H, int W, int C, int R, int S,
-                      int stride, int pad, int cpp) {
+                      int stride, int pad, int cpp, int esize = 2) {
   EncodeIm2colFn fn = encode_im2col_fn();
   if (!fn) return false;
   cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
-  cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+  cuuint64_t strides[3] = {(cuuint64_t)C * esize, (cuuint64_t)W * C * esize,
+                           (cuuint64_t)H * W * C * esize};
   int lower[2] = {-pad, -pad};
   int upper[2] = {pad - (S - 1), pad - (R - 1)};
   cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
-  if (fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, lower,
-         upper, (cuuint32_t)cpp, 128, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-         cpp == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+  if (fn(m, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+         const_cast<void*>(base), dims, strides, lower, upper, (cuuint32_t)cpp, 128, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE,
+         cpp * esize == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
+  const int esz_total = esize;
+  (void)esz_total;
   // driver <= 13.1 workaround for tensors under 128 KB (mirrors CUTLASS)
   int drv = 0;
   cudaDriverGetVersion(&drv);
-  if (drv <= 13010 && (uint64_t)N * H * W * C * 2 < 131072)
+  if (drv <= 13010 && (uint64_t)N * H * W * C * esize < 131072)
     reinterpret_cast<uint64_t*>(m)[1] &= ~(1ull << 21);
   return true;
 }
@@ -205,6 +224,7 @@ struct Layer {
   int pool_op = -1;         // s2d stem: index of the 3x3/s2 max-pool fused into its epilogue
   int ds_op = -1;           // 1x1 conv: index of the projection shortcut folded into its K loop
   int chain_op = -1;        // block-tail 1x1 conv: next block's 1x1 conv computed in the same kernel
+  bool tf32 = false;        // fp32 plan conv/linear on the 3xTF32 tcgen05 GEMM (w = hi, w2 = lo)
   bool band8 = false;       // 3x3/s1 conv on an 8-channel padded image: conv_band CGW = 8,
                             // weights [N][r][4][8] (paired taps, 4th tap zero)
   bool fused = false;       // max-pool executed inside its producer (no launch)
@@ -276,6 +296,7 @@ struct b2_plan {
   long pair_min_m = 4096;    // B2_PAIR_MIN_M: smallest M sent to the CTA-pair GEMM
   int pair_min_k = 1024;     // B2_PAIR_MIN_K: shortest K sent to the CTA-pair GEMM
   bool use_pool_fusion = true;   // B2_POOL_FUSION=0 -> stem and max-pool as two kernels
+  bool use_tf32 = true;          // B2_TF32=0 -> fp32 plans on the CUDA-core FFMA GEMM
   bool use_ds_fold = true;       // B2_DS_FOLD=0 -> projection shortcuts as their own kernels
   bool alt_order = true;         // B2_ALT_ORDER=0 -> every GEMM walks M tiles forward
   bool use_split = true;         // B2_SPLIT=0 -> no split-K at small batch
@@ -585,6 +606,28 @@ int upload_weights(b2_plan* pl, const uint8_t* data, const std::vector<WeightRec
               memcpy(&h[(size_t)r * L.kpad], w + (size_t)r * K, sizeof(float) * K);
           }
           if ((rc = upload_as<bf16>(pl, h, &L.w))) return rc;
+        } else if (!bf && !pl->force_simt && pl->use_tf32 &&
+                   ((plain && (conv ? L.p[6] : L.p[9]) % 4 == 0 && K % 4 == 0) ||
+                    (conv && L.p[6] % 32 == 0))) {
+          // 3xTF32: weights split once into hi (TF32-exact) and lo = w - hi,
+          // [N][Kpad32] fp32
+          L.tf32 = true;
+          L.kpad = (K + 31) / 32 * 32;
+          L.ldw = L.kpad;
+          std::vector<float> hi((size_t)N * L.kpad, 0.f), lo((size_t)N * L.kpad, 0.f);
+          for (int n = 0; n < N; ++n)
+            for (int k = 0; k < K; ++k) {
+              const float x = w[(size_t)n * K + k];
+              uint32_t u;
+              memcpy(&u, &x, 4);
+              u &= 0xFFFFE000u;
+              float xh;
+              memcpy(&xh, &u, 4);
+              hi[(size_t)n * L.kpad + k] = xh;
+              lo[(size_t)n * L.kpad + k] = x - xh;
+            }
+          if ((rc = upload_as<float>(pl, hi, &L.w)) || (rc = upload_as<float>(pl, lo, &L.w2)))
+            return rc;
         } else {
           L.ldw = K;
           std::vector<float> h(w, w + (size_t)N * K);
@@ -722,7 +765,33 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
         const int res_t = conv ? p[15] : p[8];
         const int act = conv ? p[14] : p[7];
         T* out = A(p[1]);
-        if (L.tc && S.chain[li]) {
+        if (L.tf32) {
+          const bool plain = !conv || (p[8] == 1 && p[9] == 1 && p[10] == 1 && p[11] == 0);
+          TcArgs a{};
+          a.nsplit = 1;
+          a.M = (int)M;
+          a.N = N;
+          a.kblocks = L.kpad / 32;
+          a.bias = L.bias;
+          a.res = res_t >= 0 ? reinterpret_cast<const bf16*>(S.act[res_t]) : nullptr;  // fp32 data
+          a.ldres = N;
+          a.out = reinterpret_cast<bf16*>(out);   // fp32 data
+          a.ldo = N;
+          a.act = act;
+          a.tiles_m = (int)((M + 127) / 128);
+          a.tiles_n = (N + 127) / 128;
+          if (!plain) {
+            a.a_im2col = 1;
+            a.C = p[6];
+            a.R = p[8];
+            a.S = p[9];
+            a.OW = p[13];
+            a.OHW = p[12] * p[13];
+            a.stride = p[10];
+            a.pad = p[11];
+          }
+          CK(tf32_gemm_launch(a, S.tmA[li], S.tmB[li], S.tmI[li], pl->num_sms, st));
+        } else if (L.tc && S.chain[li]) {
           ChainArgs ca = S.cargs[li];
           ca.reverse = pl->alt_order ? (launches & 1) : 0;
           CK(chain_launch(ca, S.tmA[li], S.tmB[li], S.tmR[li], S.tmI[li], S.tmB2[li], S.tmO[li],
@@ -1123,6 +1192,28 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
   S.bargs.resize(pl->layers.size());
   for (size_t li = 0; li < pl->layers.size(); ++li) {
     Layer& L = pl->layers[li];
+    if (L.tf32) {
+      const int* p = L.p;
+      const bool conv = L.kind == OP_CONV;
+      const int N = conv ? p[7] : p[5];
+      const long M = conv ? (long)batch * p[12] * p[13] : (long)batch * p[6];
+      const bool plain = !conv || (p[8] == 1 && p[9] == 1 && p[10] == 1 && p[11] == 0);
+      bool ok;
+      if (plain) {
+        const long ld = conv ? p[6] : p[9];
+        ok = make_tmap_f32(&S.tmA[li], S.act[p[0]], (uint64_t)M, (uint64_t)L.K,
+                           (uint64_t)ld * 4, 128);
+      } else {
+        ok = make_tmap_im2col(&S.tmA[li], S.act[p[0]], batch, p[4], p[5], p[6], p[8], p[9],
+                              p[10], p[11], 32, 4);
+      }
+      ok = ok && make_tmap_f32(&S.tmB[li], L.w, (uint64_t)N, (uint64_t)L.kpad,
+                               (uint64_t)L.kpad * 4, 128) &&
+           make_tmap_f32(&S.tmI[li], L.w2, (uint64_t)N, (uint64_t)L.kpad, (uint64_t)L.kpad * 4,
+                         128);
+      if (!ok) return fail(B2_ERR_CUDA, "layer %zu: 3xTF32 tensor maps rejected", li);
+      continue;
+    }
     if (!L.tc) continue;
     const int* p = L.p;
     int brc = plan_band(pl, S, li, batch);
@@ -1348,6 +1439,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* pm = getenv("B2_PAIR_MIN_M")) pl->pair_min_m = atol(pm);
   if (const char* pk = getenv("B2_PAIR_MIN_K")) pl->pair_min_k = atoi(pk);
   if (const char* pf = getenv("B2_POOL_FUSION")) pl->use_pool_fusion = pf[0] != '0';
+  if (const char* tf = getenv("B2_TF32")) pl->use_tf32 = tf[0] != '0';
   if (const char* df = getenv("B2_DS_FOLD")) pl->use_ds_fold = df[0] != '0';
   if (const char* ao = getenv("B2_ALT_ORDER")) pl->alt_order = ao[0] != '0';
   if (const char* sk = getenv("B2_SPLIT")) pl->use_split = sk[0] != '0';

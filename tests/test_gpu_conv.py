@@ -305,3 +305,35 @@ def test_split_k(gpu_required, monkeypatch, M, K, N, res, split):
 def test_split_k_conv(gpu_required, batch):
     """layer4 3x3 (K = 4608) at small batch: im2col A under split-K."""
     check(conv_plan(7, 7, 512, 512, 3, 1), batch)
+
+
+def check_fp32(blob, batch, seed=3):
+    pl = P.decode(blob)
+    x = plan_ref.make_inputs(pl, batch, seed)
+    plan = R.Plan(blob, P.DT_FP32)
+    try:
+        out = plan.predict(x)
+        assert np.isfinite(out).all()
+        rt = lambda t: plan.read_tensor(batch, t, pl.tensors[t].elems, pl.tensors[t].kind)
+        errs = plan_ref.layerwise_errors(pl, rt, x, False)
+        bad = [e for e in errs if not e[2] <= 1e-5]
+        assert not bad, bad
+    finally:
+        plan.close()
+
+
+@pytest.mark.parametrize("kind,args,batch", [
+    ("linear", (1024, 256, True), 300),        # plain GEMM + residual, ragged M
+    ("linear", (768, 3072, False), 64),
+    ("linear", (2048, 1000, False), 5),        # ragged N tile
+    ("conv", (14, 14, 256, 256, 3, 1), 6),     # im2col A (3x3), 72 K blocks
+    ("conv", (28, 28, 128, 256, 3, 2), 3),     # strided im2col
+    ("conv", (56, 56, 64, 64, 1, 1), 2),
+])
+@pytest.mark.parametrize("tf32", ["1", "0"])
+def test_fp32_3xtf32(gpu_required, monkeypatch, kind, args, batch, tf32):
+    """fp32 plans: 3xTF32 tcgen05 GEMM (hi/lo split, chunked TMEM partial sums)
+    vs the CUDA-core FFMA path, layerwise within 1e-5 of fp64."""
+    monkeypatch.setenv("B2_TF32", tf32)
+    blob = linear_plan(*args) if kind == "linear" else conv_plan(*args)
+    check_fp32(blob, batch)

@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python -m pytest tests/test_gpu_conv.py -x -q -k "pointwise" 2>&1 | tail -1
-timeout 600 python -m pytest tests/test_gpu.py -x -q -k "mobilenet" 2>&1 | tail -1
-for pw in 0 1; do B2_PWS=$pw timeout 120 python tools/profile_ops.py mobilenet_v2 256 > gpurun_out/mb$pw.log 2>&1; head -1 gpurun_out/mb$pw.log; done
+timeout 600 python tools/dbg_layerwise.py resnet50 0 2>&1 | tail -2
+timeout 900 python -m pytest tests/test_gpu.py -x -q -k "parity" 2>&1 | tail -2
+MICRO_DTYPE=0 timeout 120 python tools/gemm_micro.py 16384 4096 4096
+timeout 300 python tools/profile_ops.py resnet50 64 0 | head -1

@@ -18,9 +18,10 @@ y = b.tensor(N)
 b.op_p(P.OP_LINEAR, [x, y, b.weight(rng.standard_normal((N, K)) * 0.1), b.weight(np.zeros(N)), K, N, 1, 1, r, K])
 b.out_elems = b.tensors[y].elems
 b.op_p(P.OP_OUTPUT, [1, b.tensor(1) if False else y, 0])
+DT = int(os.environ.get("MICRO_DTYPE", P.DT_BF16))
 blob = b.build(P.DT_BF16)
-plan = R.Plan(blob, P.DT_BF16)
+plan = R.Plan(blob, DT)
 prof = plan.profile_ops(M, iters=5)
 ms = prof[-2][1]
-byts = 2 * M * (K + N * (2 if res else 1))
+byts = (2 if DT == P.DT_BF16 else 4) * M * (K + N * (2 if res else 1))
 print(f"M={M} K={K} N={N} res={res} mode={os.environ.get('B2_EPI_MODE','0')} stages={os.environ.get('B2_STAGES','auto')}: {ms*1e3:.1f} us  {2*M*N*K/ms/1e9:.1f} TF/s  {byts/ms/1e6:.0f} GB/s")
