@@ -492,9 +492,11 @@ template <int ACT>
 static cudaError_t band_dispatch(const BandArgs& a, int bn, int cgw, const CUtensorMap& ta,
                                  const CUtensorMap& tb, const CUtensorMap& to,
                                  const CUtensorMap& to2, int num_sms, cudaStream_t st) {
-  if (cgw == 16) {   // space-to-depth 7x7/2 stem: 4 x 4 taps, resident weights
+  if (cgw == 16) {   // space-to-depth stems: 7x7/2 -> 4 x 4 taps, 3x3/2 -> 2 x 4
     if (bn == 64 && a.R == 4 && a.S == 4 && a.b_resident && a.CG == 1)
       return band_launch_t<64, 16, 4, 4, true, ACT>(a, ta, tb, to, to2, num_sms, st);
+    if (bn == 64 && a.R == 2 && a.S == 4 && a.b_resident && a.CG == 1)
+      return band_launch_t<64, 16, 2, 4, true, ACT>(a, ta, tb, to, to2, num_sms, st);
     return cudaErrorInvalidValue;
   }
   if (cgw == 8) {    // 3x3 on an 8-channel padded image (VGG conv1_1)
@@ -517,8 +519,10 @@ static cudaError_t band_dispatch(const BandArgs& a, int bn, int cgw, const CUten
 
 // Which (taps, BN, residency) combinations have a kernel instance.
 bool band_supported(const BandArgs& a, int bn, int cgw, int act) {
-  if (act != ACT_NONE && act != ACT_RELU) return false;
-  if (cgw == 16) return bn == 64 && a.R == 4 && a.S == 4 && a.b_resident && a.CG == 1;
+  if (act != ACT_NONE && act != ACT_RELU && !(act == ACT_RELU6 && cgw == 16)) return false;
+  if (cgw == 16)
+    return bn == 64 && (a.R == 4 || a.R == 2) && a.S == 4 && a.b_resident && a.CG == 1 &&
+           (act != ACT_RELU6 || a.R == 2);
   if (cgw == 8) return bn == 64 && a.R == 3 && a.S == 3 && a.b_resident && a.CG == 1;
   if (a.R != 3 || a.S != 3) return false;
   if (a.b_resident) return bn == 64 && a.CG == 1;
@@ -530,6 +534,8 @@ cudaError_t conv_band_launch(const BandArgs& a, int bn, int cgw, const CUtensorM
                              int num_sms, cudaStream_t st) {
   if (a.act == ACT_RELU) return band_dispatch<ACT_RELU>(a, bn, cgw, ta, tb, to, to2, num_sms, st);
   if (a.act == ACT_NONE) return band_dispatch<ACT_NONE>(a, bn, cgw, ta, tb, to, to2, num_sms, st);
+  if (a.act == ACT_RELU6 && cgw == 16 && bn == 64 && a.R == 2 && a.S == 4 && a.b_resident)
+    return band_launch_t<64, 16, 2, 4, true, ACT_RELU6>(a, ta, tb, to, to2, num_sms, st);
   return cudaErrorInvalidValue;
 }
 

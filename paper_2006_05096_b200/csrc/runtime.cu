@@ -1048,10 +1048,13 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
   BandArgs a{};
   int cgw = 64;
   if (L.s2d) {
-    if (N % 64 != 0 || N > 128) return 0;
+    // N = 32 (MobileNetV2 stem) runs as a 64-wide tile: weight rows 32..63 are
+    // TMA zero-fill and the output map clips columns >= 32
+    if ((N % 64 != 0 && N != 32) || N > 128) return 0;
     cgw = 16;
     a.Wp = band_pitch(L.s2d_W2);
-    a.R = a.S = L.s2d_Rp;
+    a.R = L.s2d_Rp;
+    a.S = 4;   // the s2d weight layout always holds 4 columns of 16 (zeros past the filter)
     a.CG = 1;
     a.x0 = a.y0 = 0;
   } else if (L.band8) {
@@ -1080,7 +1083,7 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
   a.W = OW;
   a.N = N;
   a.kblocks = L.kpad / 64;
-  a.tiles_n = N / bn;
+  a.tiles_n = (N + bn - 1) / bn;
   a.out = reinterpret_cast<bf16*>(S.act[p[1]]);
   a.act = p[14];
   a.bias = L.bias ? L.bias : pl->zero_bias;

@@ -80,6 +80,15 @@ def test_stem_s2d(gpu_required, batch):
     check(conv_plan(224, 224, 3, 64, 7, 2), batch)
 
 
+@pytest.mark.parametrize("N,act,batch", [(32, 2, 1), (32, 2, 8), (64, 1, 3), (32, 0, 2)])
+def test_stem_s2d_3x3(gpu_required, monkeypatch, N, act, batch):
+    """3x3/2 stem (MobileNetV2: 3 -> 32, ReLU6): space-to-depth band path with
+    2 x 4 taps and a half-empty 64-wide tile, then the s2d GEMM path."""
+    check(conv_plan(224, 224, 3, N, 3, 2, act=act), batch)
+    monkeypatch.setenv("B2_BAND", "0")
+    check(conv_plan(224, 224, 3, N, 3, 2, act=act), batch)
+
+
 @pytest.mark.parametrize("k,stride,H,C,N", [(3, 2, 28, 128, 128), (1, 2, 28, 256, 512),
                                              (5, 1, 14, 64, 64)])
 def test_other_convs(gpu_required, k, stride, H, C, N):
