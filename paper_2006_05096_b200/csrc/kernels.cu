@@ -337,6 +337,145 @@ __global__ void __launch_bounds__(256) dwconv3_vec_kernel(const T* __restrict__ 
   *reinterpret_cast<uint4*>(y + ((b * OH + oh) * OW + ow) * (long)C + c0) = ov.u;
 }
 
+// acc + x[k] * w[k] for element k of two 16-byte vectors. bf16 uses the
+// mixed-precision FMA (fma.rn.f32.bf16 -> FHFMA.BF16 with .H1 half selects):
+// bf16 x bf16 is exact in fp32, so this equals fmaf on the widened values but
+// needs no conversion instructions.
+template <typename T> struct DwFma;
+template <> struct DwFma<float> {
+  static B2_DEV float f(const Vec16<float>& x, const Vec16<float>& w, int k, float acc) {
+    return fmaf(x.e[k], w.e[k], acc);
+  }
+};
+template <> struct DwFma<bf16> {
+  static B2_DEV float f(const Vec16<bf16>& x, const Vec16<bf16>& w, int k, float acc) {
+    const uint32_t xs = (&x.u.x)[k >> 1], ws = (&w.u.x)[k >> 1];
+    unsigned short xl, xh, wl, wh;
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(xl), "=h"(xh) : "r"(xs));
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(wl), "=h"(wh) : "r"(ws));
+    float d;
+    if (k & 1)
+      asm("fma.rn.f32.bf16 %0, %1, %2, %3;" : "=f"(d) : "h"(xh), "h"(wh), "f"(acc));
+    else
+      asm("fma.rn.f32.bf16 %0, %1, %2, %3;" : "=f"(d) : "h"(xl), "h"(wl), "f"(acc));
+    return d;
+  }
+};
+
+// Row-strip variant: one thread = one 16-byte channel vector x OWT adjacent
+// outputs of one row. The 9 filter taps stay in registers for the strip and
+// each input column is loaded once per filter row for all OWT outputs, so L1
+// traffic per output drops from 18 to (3*(STRIDE*(OWT-1)+3) + 9) / OWT vectors.
+// Index math is 32-bit (the flat kernel's 64-bit divides were most of its
+// instruction stream). Out-of-image rows are skipped; strips touching the left
+// or right image edge take a clamped, zero-filled load path.
+template <typename T, int STRIDE, int ACT, int OWT>
+__global__ void __launch_bounds__(256) dwconv3_strip_kernel(const T* __restrict__ x,
+                                                            const T* __restrict__ w,
+                                                            const float* __restrict__ bias,
+                                                            T* __restrict__ y, int B, int H, int W,
+                                                            int C, int OH, int OW, int NS) {
+  constexpr int V = Vec16<T>::N;
+  constexpr int IW = STRIDE * (OWT - 1) + 3;
+  const int CV = C / V;
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (unsigned)(B * OH * NS * CV)) return;
+  const int cv = (int)(i % (unsigned)CV);
+  const unsigned rest = i / (unsigned)CV;
+  const int strip = (int)(rest % (unsigned)NS);
+  const unsigned row = rest / (unsigned)NS;   // b * OH + oh
+  const int oh = (int)(row % (unsigned)OH);
+  const int b = (int)(row / (unsigned)OH);
+  const int c0 = cv * V;
+  const int ow0 = strip * OWT;
+  const int iw0 = ow0 * STRIDE - 1;
+  const bool interior = iw0 >= 0 && iw0 + IW <= W;
+  float acc[OWT][V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const float bv = bias ? __ldg(bias + c0 + k) : 0.f;
+#pragma unroll
+    for (int o = 0; o < OWT; ++o) acc[o][k] = bv;
+  }
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int ih = oh * STRIDE - 1 + r;
+    if ((unsigned)ih >= (unsigned)H) continue;
+    Vec16<T> wv[3];
+#pragma unroll
+    for (int s = 0; s < 3; ++s)
+      wv[s].u = __ldg(reinterpret_cast<const uint4*>(w + (r * 3 + s) * C + c0));
+    const T* xrow = x + ((size_t)(b * H + ih) * W) * C + c0;
+    Vec16<T> xv[IW];
+    if (interior) {
+      const uint4* p = reinterpret_cast<const uint4*>(xrow + (size_t)iw0 * C);
+      const int cs = C / V;   // uint4 stride between columns
+#pragma unroll
+      for (int j = 0; j < IW; ++j) xv[j].u = __ldg(p + j * cs);
+    } else {
+#pragma unroll
+      for (int j = 0; j < IW; ++j) {
+        const int iw = iw0 + j;
+        const int iwc = min(max(iw, 0), W - 1);
+        xv[j].u = __ldg(reinterpret_cast<const uint4*>(xrow + (size_t)iwc * C));
+        if ((unsigned)iw >= (unsigned)W) xv[j].u = make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < IW; ++j)
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+#pragma unroll
+        for (int o = 0; o < OWT; ++o) {
+          const int s = j - o * STRIDE;
+          if (s >= 0 && s < 3) acc[o][k] = DwFma<T>::f(xv[j], wv[s], k, acc[o][k]);
+        }
+  }
+  T* yrow = y + ((size_t)row * OW + ow0) * C + c0;
+#pragma unroll
+  for (int o = 0; o < OWT; ++o) {
+    if (ow0 + o >= OW) break;
+    Vec16<T> ov;
+#pragma unroll
+    for (int k = 0; k < V; ++k) ov.e[k] = from_f<T>(act_t<ACT>(acc[o][k]));
+    *reinterpret_cast<uint4*>(yrow + (size_t)o * C) = ov.u;
+  }
+}
+
+// Strip width (measured on MobileNetV2 b=256: stride 1 best at 4, stride 2 at 2;
+// B2_DW_OWT / B2_DW_OWT2 override, 1 = the flat per-output kernel)
+static int dw_owt(int stride) {
+  static int v1 = [] {
+    const char* e = getenv("B2_DW_OWT");
+    return e ? atoi(e) : 4;
+  }();
+  static int v2 = [] {
+    const char* e = getenv("B2_DW_OWT2");
+    return e ? atoi(e) : 2;
+  }();
+  return stride == 1 ? v1 : v2;
+}
+
+template <typename T, int STRIDE, int OWT>
+static cudaError_t dwconv3_strip_launch(const T* x, const T* w, const float* bias, T* y, int B,
+                                        int H, int W, int C, int OH, int OW, int act,
+                                        cudaStream_t st) {
+  const int NS = (OW + OWT - 1) / OWT;
+  const long total = (long)B * OH * NS * (C / Vec16<T>::N);
+  switch (act) {
+#define B2_DW3S(A)                                                                             \
+  case A:                                                                                      \
+    dwconv3_strip_kernel<T, STRIDE, A, OWT><<<nblk(total, 256), 256, 0, st>>>(            \
+        x, w, bias, y, B, H, W, C, OH, OW, NS);                                                \
+    return cudaGetLastError();
+    B2_DW3S(ACT_NONE)
+    B2_DW3S(ACT_RELU)
+    B2_DW3S(ACT_RELU6)
+#undef B2_DW3S
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <typename T, int STRIDE>
 static cudaError_t dwconv3_launch(const T* x, const T* w, const float* bias, T* y, int B, int H,
                                   int W, int C, int OH, int OW, int act, cudaStream_t st) {
@@ -358,6 +497,21 @@ static cudaError_t dwconv3_launch(const T* x, const T* w, const float* bias, T* 
 template <typename T>
 cudaError_t dwconv(const T* x, const T* w, const float* bias, T* y, int B, int H, int W, int C,
                    int R, int stride, int pad, int OH, int OW, int act, cudaStream_t st) {
+  if (C % Vec16<T>::N == 0 && R == 3 && pad == 1 && (stride == 1 || stride == 2) &&
+      (act == ACT_NONE || act == ACT_RELU || act == ACT_RELU6)) {
+    const int owt = dw_owt(stride);
+    const long rows = (long)B * OH * (C / Vec16<T>::N);
+    if (stride == 1 && owt == 8 && rows * ((OW + 7) / 8) < (1L << 31))
+      return dwconv3_strip_launch<T, 1, 8>(x, w, bias, y, B, H, W, C, OH, OW, act, st);
+    if (stride == 1 && owt == 4 && rows * ((OW + 3) / 4) < (1L << 31))
+      return dwconv3_strip_launch<T, 1, 4>(x, w, bias, y, B, H, W, C, OH, OW, act, st);
+    if (stride == 2 && owt == 4 && rows * ((OW + 3) / 4) < (1L << 31))
+      return dwconv3_strip_launch<T, 2, 4>(x, w, bias, y, B, H, W, C, OH, OW, act, st);
+    if (owt == 2 && rows * ((OW + 1) / 2) < (1L << 31))
+      return stride == 1
+                 ? dwconv3_strip_launch<T, 1, 2>(x, w, bias, y, B, H, W, C, OH, OW, act, st)
+                 : dwconv3_strip_launch<T, 2, 2>(x, w, bias, y, B, H, W, C, OH, OW, act, st);
+  }
   if (C % Vec16<T>::N == 0 && R == 3 && pad == 1 && (stride == 1 || stride == 2) &&
       (act == ACT_NONE || act == ACT_RELU || act == ACT_RELU6))
     return stride == 1 ? dwconv3_launch<T, 1>(x, w, bias, y, B, H, W, C, OH, OW, act, st)
