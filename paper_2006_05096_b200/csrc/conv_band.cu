@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
         const int p0 = mt * 128 + q * 32;               // band position of lane 0
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + ab * a.MT * BN + mt * BN;
 #pragma unroll 1
-        for (int c = eh * 32; c < BN; c += 64) {
+        for (int c = eh * 32; c < BN && n0 + c < a.N; c += 64) {   // columns >= N: nothing to store
           uint32_t rr[32];
           tmem_ld_32x32b_x32(taddr + c, rr);
           float bv[32];

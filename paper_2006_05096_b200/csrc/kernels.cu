@@ -442,13 +442,15 @@ __global__ void __launch_bounds__(256) dwconv3_strip_kernel(const T* __restrict_
   }
 }
 
-// Strip width (measured on MobileNetV2 b=256: stride 1 best at 4, stride 2 at 2;
+// Strip width (measured on MobileNetV2 b=256: stride 1 best at 8 when the row
+// splits into whole strips of 8 (or is short), else 4; stride 2 best at 2;
 // B2_DW_OWT / B2_DW_OWT2 override, 1 = the flat per-output kernel)
-static int dw_owt(int stride) {
+static int dw_owt(int stride, int OW) {
   static int v1 = [] {
     const char* e = getenv("B2_DW_OWT");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 0;
   }();
+  if (stride == 1 && v1 == 0) return (OW % 8 == 0 || OW < 16) ? 8 : 4;
   static int v2 = [] {
     const char* e = getenv("B2_DW_OWT2");
     return e ? atoi(e) : 2;
@@ -499,7 +501,7 @@ cudaError_t dwconv(const T* x, const T* w, const float* bias, T* y, int B, int H
                    int R, int stride, int pad, int OH, int OW, int act, cudaStream_t st) {
   if (C % Vec16<T>::N == 0 && R == 3 && pad == 1 && (stride == 1 || stride == 2) &&
       (act == ACT_NONE || act == ACT_RELU || act == ACT_RELU6)) {
-    const int owt = dw_owt(stride);
+    const int owt = dw_owt(stride, OW);
     const long rows = (long)B * OH * (C / Vec16<T>::N);
     if (stride == 1 && owt == 8 && rows * ((OW + 7) / 8) < (1L << 31))
       return dwconv3_strip_launch<T, 1, 8>(x, w, bias, y, B, H, W, C, OH, OW, act, st);
