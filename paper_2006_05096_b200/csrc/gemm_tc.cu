@@ -890,6 +890,55 @@ int tc_pick_split(long tiles, int kt, int num_sms) {
   return sp < 2 ? 1 : sp;
 }
 
+// Tile shape + kernel (single CTA vs CTA pair) from a per-SM clock model.
+// Per 64-wide K block a tile costs max(MMA, operand bytes / TMA rate): the
+// chip's TMA/L2 fill rate (~12 TB/s measured, ~42 B/clk per SM) is below what
+// a 128 x 256 tile's MMAs consume (48 KB per 512 MMA clocks), so the CTA pair
+// -- each CTA loads its own A rows but only half of B -- runs long-K shapes
+// ~1.5x faster. The epilogue (~10.5 B/clk of output per SM) overlaps the next
+// tile's mainloop, so short-K tiles cost max(mainloop, epilogue).
+// Measured at M = 16384, K = 768: N = 2304 62.8 -> 50.2 us, N = 3072 (was
+// BN = 128 single) 127 -> see DESIGN.md; K = 256 N = 1024 stays single.
+static double tc_tile_clk(int bn, bool pair, int kblocks, int nvalid) {
+  const double mma = 4.0 * (bn > 128 ? 128 : 64);
+  const double bytes = 16384.0 + (pair ? bn / 2 : bn) * 128.0;
+  const double mainloop = kblocks * (mma > bytes / 42.0 ? mma : bytes / 42.0);
+  const double epi = 128.0 * (nvalid < bn ? nvalid : bn) * 2.0 / 10.5;
+  // + ~600 clk per tile of barrier round trips / TMEM hand-off / pipeline
+  // refill that no overlap hides (keeps narrow tiles from winning ties)
+  return (mainloop > epi ? mainloop : epi) + 600.0;
+}
+
+int tc_pick_config(long M, int N, int kblocks, bool res_fold, int num_sms, bool pair_allowed,
+                   bool* pair_out) {
+  const int cands[5] = {256, 128, 64, 32, 16};
+  double best_cost = -1;
+  int best = 16;
+  bool best_pair = false;
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool pair = pass == 1;
+    if (pair && !pair_allowed) break;
+    for (int bn : cands) {
+      if (pair && bn < 128) continue;
+      if (bn > 16 && bn / 2 >= N && !(bn == 32 && N % 8 == 0 && N >= 8)) continue;
+      if (bn == 16 && N % 8 == 0) continue;   // BN = 32 gets the TMA-store epilogue
+      const long tm = pair ? (M + 2 * TC_BM - 1) / (2 * TC_BM) : (M + TC_BM - 1) / TC_BM;
+      const long tn = (N + bn - 1) / bn;
+      const long slots = pair ? num_sms / 2 : num_sms;
+      const long waves = (tm * tn + slots - 1) / slots;
+      const int kb = kblocks + (res_fold ? (bn >= 64 ? bn / 64 : 1) : 0);
+      const double cost = waves * tc_tile_clk(bn, pair, kb, (int)(N / tn));   // mean valid cols
+      if (best_cost < 0 || cost < best_cost * 0.999) {
+        best_cost = cost;
+        best = bn;
+        best_pair = pair;
+      }
+    }
+  }
+  *pair_out = best_pair;
+  return best;
+}
+
 int tc_pick_bn(long M, int N, int num_sms) {
   const int cands[5] = {256, 128, 64, 32, 16};
   long best_cost = -1;

@@ -99,6 +99,9 @@ cudaError_t chain_launch(const ChainArgs& a, const CUtensorMap& tA, const CUtens
                          cudaStream_t st);
 
 int tc_pick_bn(long M, int N, int num_sms);
+// BN and single-CTA vs CTA-pair kernel from the per-SM clock model (gemm_tc.cu)
+int tc_pick_config(long M, int N, int kblocks, bool res_fold, int num_sms, bool pair_allowed,
+                   bool* pair_out);
 cudaError_t tf32_gemm_launch(const TcArgs& a, const CUtensorMap& ta, const CUtensorMap& tbh,
                              const CUtensorMap& tbl, int num_sms, cudaStream_t st);
 int tc_pick_split(long tiles, int kt, int num_sms);

@@ -293,8 +293,9 @@ struct b2_plan {
                              // (correct, but issue-bound on 2 KB boxes: slower than gather)
   bool use_band = true;      // B2_BAND=0 -> stride-1 k x k convs and s2d stems on gemm_tc
   bool use_pair = true;      // B2_PAIR=0 -> single-CTA tc_gemm only
+  bool verbose = false;      // B2_VERBOSE=1: per-layer kernel choices on stderr
   long pair_min_m = 4096;    // B2_PAIR_MIN_M: smallest M sent to the CTA-pair GEMM
-  int pair_min_k = 1024;     // B2_PAIR_MIN_K: shortest K sent to the CTA-pair GEMM
+  int pair_min_k = 0;        // B2_PAIR_MIN_K: shortest K sent to the CTA-pair GEMM
   bool use_pool_fusion = true;   // B2_POOL_FUSION=0 -> stem and max-pool as two kernels
   bool use_tf32 = true;          // B2_TF32=0 -> fp32 plans on the CUDA-core FFMA GEMM
   bool use_ds_fold = true;       // B2_DS_FOLD=0 -> projection shortcuts as their own kernels
@@ -847,7 +848,7 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
           a.ts_debug = pl->ts_debug;
           a.stages = pl->stages_override;
           a.reverse = pl->alt_order ? (launches & 1) : 0;
-          a.res_kblocks = S.fold[li] ? bn / 64 : 0;
+          a.res_kblocks = S.fold[li] ? (bn >= 64 ? bn / 64 : 1) : 0;   // BN 32: one 64-wide block, identity rows [0, 32)
           if (S.fold[li] >= 2) {
             const int* q = pl->layers[L.ds_op].p;
             a.res_kblocks = pl->layers[L.ds_op].kpad / 64;
@@ -1236,16 +1237,16 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     const bool conv = L.kind == OP_CONV;
     const int N = conv ? p[7] : p[5];
     const long M = conv ? (long)batch * p[12] * p[13] : (long)batch * p[6];
-    // CTA-pair (cta_group::2) GEMM for the TMA-fed shapes big enough to fill
-    // the pairs; weight boxes then hold BN/2 rows (each CTA loads half)
-    // measured (tools/gemm_sweep.sh): pairs win on long-K, wide-N GEMMs
-    // (K >= 1024, BN = 256: +7% at 16384x4096x4096, +7% at 50176x1024x256)
-    // and lose on short-K / residual-fold / BN = 128 shapes
-    const bool pair_ok = pl->use_pair && !L.s2d && !L.gather && L.ds_op < 0 &&
-                         (!L.im2col || L.im2col_mode == 1) &&
-                         N % 8 == 0 && M >= pl->pair_min_m && L.K >= pl->pair_min_k &&
-                         tc2_pick_bn(M, N, pl->num_sms) == 256;
-    int bn = pair_ok ? tc2_pick_bn(M, N, pl->num_sms) : tc_pick_bn(M, N, pl->num_sms);
+    // CTA-pair (cta_group::2) GEMM vs single CTA and the tile width: per-SM
+    // clock model in tc_pick_config (TMA fill rate vs MMA vs epilogue writes).
+    // Pairs need a TMA-fed A (no gather / s2d / folded shortcut).
+    const bool pair_allowed = pl->use_pair && !L.s2d && !L.gather && L.ds_op < 0 &&
+                              (!L.im2col || L.im2col_mode == 1) && N % 8 == 0 &&
+                              M >= pl->pair_min_m && L.K >= pl->pair_min_k;
+    const int res_in = conv ? p[15] : p[8];
+    bool pair_ok = false;
+    int bn = tc_pick_config(M, N, L.kpad / 64, res_in >= 0 && L.K <= pl->fold_max_k,
+                            pl->num_sms, pair_allowed, &pair_ok);
     // Memory-bound shapes (one K block, or im2col A that each extra N tile
     // re-gathers) want the widest tile: measured 56x56x64->256 128 -> 115 us,
     // 56x56x256->28x28x512/s2 110 -> 72 us with BN = 256 instead of 128.
@@ -1253,6 +1254,9 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     if (pl->force_bn && !pair_ok && N % pl->force_bn == 0) bn = pl->force_bn;   // B2_FORCE_BN (tuning aid)
     S.bn[li] = bn;
     S.pair[li] = pair_ok;
+    if (pl->verbose)
+      fprintf(stderr, "b2: layer %zu M=%ld N=%d K=%d kpad=%d -> bn=%d pair=%d\n", li, M, N, L.K,
+              L.kpad, bn, (int)pair_ok);
     if (!pair_ok && !L.gather && !L.s2d && L.ds_op < 0 && bn >= 32 && N % 8 == 0 &&
         pl->use_split && pl->epi_mode == 0) {
       const long tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
@@ -1312,7 +1316,7 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
                                  (uint64_t)D.kpad * 2, bbox))
         return fail(B2_ERR_CUDA, "layer %zu: folded shortcut tensor maps rejected", li);
       S.fold[li] = q[10] == 1 ? 2 : 3;
-    } else if (res_t >= 0 && bn >= 64 && N % 8 == 0 && L.K <= pl->fold_max_k && pl->identity &&
+    } else if (res_t >= 0 && bn >= 32 && N % 8 == 0 && L.K <= pl->fold_max_k && pl->identity &&
                S.split[li] == 1) {   // split-K adds the residual in its finalize pass
       if (!make_tmap_bf16(&S.tmR[li], S.act[res_t], (uint64_t)M, (uint64_t)N, (uint64_t)N * 2,
                           128) ||
@@ -1439,6 +1443,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* sd = getenv("B2_S2D")) pl->use_s2d = sd[0] != '0';
   if (const char* bd = getenv("B2_BAND")) pl->use_band = bd[0] != '0';
   if (const char* pr = getenv("B2_PAIR")) pl->use_pair = pr[0] != '0';
+  if (const char* vb = getenv("B2_VERBOSE")) pl->verbose = vb[0] == '1';
   if (const char* pm = getenv("B2_PAIR_MIN_M")) pl->pair_min_m = atol(pm);
   if (const char* pk = getenv("B2_PAIR_MIN_K")) pl->pair_min_k = atoi(pk);
   if (const char* pf = getenv("B2_POOL_FUSION")) pl->use_pool_fusion = pf[0] != '0';

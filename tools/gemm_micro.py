@@ -15,7 +15,8 @@ if res:
     r = b.tensor(N)
     b.op_p(P.OP_LINEAR, [x, r, b.weight(rng.standard_normal((N, K)) * 0.1), b.weight(np.zeros(N)), K, N, 1, 0, -1, K])
 y = b.tensor(N)
-b.op_p(P.OP_LINEAR, [x, y, b.weight(rng.standard_normal((N, K)) * 0.1), b.weight(np.zeros(N)), K, N, 1, 1, r, K])
+ACT = int(os.environ.get("MICRO_ACT", 1))   # 0 none, 1 relu, 2 relu6, 3 gelu, 4 tanh
+b.op_p(P.OP_LINEAR, [x, y, b.weight(rng.standard_normal((N, K)) * 0.1), b.weight(np.zeros(N)), K, N, 1, ACT, r, K])
 b.out_elems = b.tensors[y].elems
 b.op_p(P.OP_OUTPUT, [1, b.tensor(1) if False else y, 0])
 DT = int(os.environ.get("MICRO_DTYPE", P.DT_BF16))
