@@ -152,11 +152,12 @@ def roofline(plan, plan_bytes: bytes, batch: int, pk: dict) -> dict:
     traffic = None
     tp = ROOT / "profiles" / "ncu_traffic.json"
     if tp.exists():
-        traffic = json.loads(tp.read_text()).get("tc_gemm_bytes_per_launch")
+        tj = json.loads(tp.read_text())
+        traffic = tj.get("tcgen05_bytes_per_launch", tj.get("tc_gemm_bytes_per_launch"))
     return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
             "kernel": "tcgen05 conv/GEMM kernels (tc_gemm, tc_gemm2 CTA-pair, conv_band, "
-                      "stem_pool) over every conv/linear op",
+                      "stem_pool, chain_gemm) over every conv/linear op",
             "launches_per_step": launches, "avg_launch_ms": round(t_gemm / launches, 5),
             "share_of_step": round(t_gemm / t_all, 4),
             "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({pk['_source']})"}

@@ -19,6 +19,7 @@ both without any data-path collective (cells are independent):
 from __future__ import annotations
 
 import heapq
+import math
 import threading
 import time
 from typing import Callable, Optional
@@ -37,15 +38,67 @@ def cell_cost(flops_per_sample: float, cell: Cell, requests: int, warmup: int,
     return flops_per_sample * cell.batch_size * (requests + warmup) / (tflops * 1e12) + setup_s
 
 
-def lpt_partition(items: list, cost: Callable[[object], float], k: int) -> list[list]:
-    """Longest-processing-time-first greedy partition into k bins (stable)."""
+def lpt_partition(items: list, cost: Callable[[object], float], k: int,
+                  group: Callable[[object], object] | None = None,
+                  setup: Callable[[object], float] | None = None) -> list[list]:
+    """Longest-processing-time-first greedy partition into k bins (stable).
+
+    With ``group``/``setup``: a bin pays ``setup(g)`` once for every distinct
+    group g it hosts (a model's worker start on a GPU), and each item goes to
+    the bin where its completion time -- load + cost + any new setup -- is
+    smallest, so cells of one model stay together unless splitting pays."""
     bins: list[list] = [[] for _ in range(k)]
-    heap = [(0.0, i) for i in range(k)]
-    heapq.heapify(heap)
-    for it in sorted(items, key=lambda x: -cost(x)):
-        load, i = heapq.heappop(heap)
-        bins[i].append(it)
-        heapq.heappush(heap, (load + cost(it), i))
+    if group is None or setup is None:
+        heap = [(0.0, i) for i in range(k)]
+        heapq.heapify(heap)
+        for it in sorted(items, key=lambda x: -cost(x)):
+            load, i = heapq.heappop(heap)
+            bins[i].append(it)
+            heapq.heappush(heap, (load + cost(it), i))
+        return bins
+    # two-level LPT: split each group into as many chunks as its work fills
+    # bins of the ideal makespan (total work + one setup per group) / k, then
+    # place the chunks (work + setup) longest first on the least-loaded bin
+    groups: dict = {}
+    for it in items:
+        groups.setdefault(group(it), []).append(it)
+    work = {g: sum(cost(x) for x in xs) for g, xs in groups.items()}
+    target = (sum(work.values()) + sum(setup(g) for g in groups)) / k
+    chunks = []
+    for g, xs in groups.items():
+        n = max(1, min(k, len(xs), math.ceil(work[g] / max(target, 1e-12) - 1e-9)))
+        for part in lpt_partition(xs, cost, n):
+            if part:
+                chunks.append((g, part))
+    loads = [0.0] * k
+    hosted: list[set] = [set() for _ in range(k)]
+    for g, part in sorted(chunks, key=lambda c: -(sum(cost(x) for x in c[1]) + setup(c[0]))):
+        i = min(range(k), key=lambda j: loads[j])
+        bins[i].extend(part)
+        loads[i] += sum(cost(x) for x in part) + (0.0 if g in hosted[i] else setup(g))
+        hosted[i].add(g)
+
+    def load(b):
+        return sum(cost(x) for x in b) + sum(setup(h) for h in {group(x) for x in b})
+
+    # local search: move single items off the busiest bin while that lowers it
+    for _ in range(4 * len(items)):
+        lds = [load(b) for b in bins]
+        hi = max(range(k), key=lambda j: lds[j])
+        best = None
+        for x in bins[hi]:
+            rest = [y for y in bins[hi] if y is not x]
+            for j in range(k):
+                if j == hi:
+                    continue
+                new_max = max(load(rest), load(bins[j] + [x]))
+                if new_max < lds[hi] - 1e-9 and (best is None or new_max < best[0]):
+                    best = (new_max, x, j)
+        if best is None:
+            break
+        _, x, j = best
+        bins[hi] = [y for y in bins[hi] if y is not x]
+        bins[j].append(x)
     return bins
 
 

@@ -74,6 +74,24 @@ def test_lpt_partition_balances():
         assert max(loads) <= sum(loads) / k + max(cost(u) for u in units) + 1e-9
 
 
+def test_lpt_partition_setup_aware():
+    """A bin pays each hosted model's worker start once; the setup-aware
+    greedy keeps a model's cells together unless splitting them pays."""
+    units = [("a", i) for i in range(4)] + [("b", i) for i in range(4)]
+    cost = lambda u: 1.0
+    start = {"a": 10.0, "b": 10.0}
+    bins = lpt_partition(units, cost, 2, group=lambda u: u[0], setup=lambda m: start[m])
+    assert sorted(u for b in bins for u in b) == sorted(units)
+    assert all(len({u[0] for u in b}) == 1 for b in bins)      # one model per GPU: 14 each
+    plain = lpt_partition(units, cost, 2)
+    load = lambda bs: max(sum(cost(u) for u in b) + sum(start[m] for m in {u[0] for u in b})
+                          for b in bs)
+    assert load(bins) == 14.0 < load(plain)                     # plain LPT mixes: 24
+    # cheap starts: the cells spread out like plain LPT
+    cheap = lpt_partition(units, cost, 4, group=lambda u: u[0], setup=lambda m: 0.1)
+    assert max(len(b) for b in cheap) == 2
+
+
 def _rank_main(rank, world, port, q):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))

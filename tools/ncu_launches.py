@@ -26,15 +26,16 @@ for d in fwd:
     a[2] += d.get('dram__bytes_read.sum', 0) + d.get('dram__bytes_write.sum', 0)
 lines = [f"{k:50s} launches={n:3d} time={us:9.1f} us share={100 * us / tot:5.1f}%  dram={by / 1e6:9.1f} MB"
          for k, (n, us, by) in sorted(agg.items(), key=lambda x: -x[1][1])]
-tc = [d for d in fwd if 'tc_gemm' in d['name']]
+FAMILY = ('tc_gemm', 'conv_band', 'chain_gemm', 'stem_pool')   # the tcgen05 conv/GEMM kernels
+tc = [d for d in fwd if any(f in d['name'] for f in FAMILY)]
 tb = sum(d.get('dram__bytes_read.sum', 0) + d.get('dram__bytes_write.sum', 0) for d in tc) / len(tc)
 share = sum(d['gpu__time_duration.sum'] for d in tc) / tot
 head = (f"one ResNet-50 bf16 batch-256 forward from the ncu launch list (cold cache, serialised: "
         f"compare shares, not absolutes)\ntotal {tot:.1f} us over {len(fwd)} launches; "
-        f"tc_gemm share {100 * share:.1f}%, avg DRAM traffic per tc_gemm launch {tb / 1e6:.1f} MB\n")
+        f"tcgen05 conv/GEMM share {100 * share:.1f}%, avg DRAM traffic per launch {tb / 1e6:.1f} MB\n")
 open(out_summary, 'w').write(head + "\n".join(lines) + "\n")
-json.dump({"tc_gemm_bytes_per_launch": tb, "tc_gemm_launches_per_forward": len(tc),
-           "tc_gemm_time_share_ncu": share, "forward_us_ncu": tot,
+json.dump({"tcgen05_bytes_per_launch": tb, "tcgen05_launches_per_forward": len(tc),
+           "tcgen05_time_share_ncu": share, "family": list(FAMILY), "forward_us_ncu": tot,
            "source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
                      "--clock-control none, python bench.py --steps 2 --warmup 3 --no-sweep --no-cpu"},
           open(out_json, 'w'), indent=1)

@@ -103,17 +103,22 @@ def main() -> int:
     finally:
         disp.shutdown()
     wall = time.perf_counter() - t_sweep
-    # per-model set-up on a GPU: its share of the concurrent worker start plus
-    # its cells' non-device time (graph capture, RPC)
-    setup = {m: prewarm_s / len(models) + max(0.0, per_model[m]["wall_s"] - sum(
-        c["device_s"] for c in cells if c["model"] == m)) for m in models}
+    # per-model worker start on a GPU (its share of the concurrent pre-warm) is
+    # paid once per GPU hosting the model; the rest of the model's non-device
+    # wall time (per-batch state + graph capture, RPC) is per cell and moves
+    # with the cell
+    start = {m: prewarm_s / len(models) for m in models}
+    for m in models:
+        mc = [c for c in cells if c["model"] == m]
+        extra = max(0.0, per_model[m]["wall_s"] - sum(c["device_s"] for c in mc))
+        for c in mc:
+            c["overhead_s"] = round(extra / len(mc), 4)
     proj = {}
     for k in (1, 2, 4, 8):
-        # each GPU runs its LPT share of cells; a model's worker start is paid on
-        # every GPU that hosts one of its cells
-        bins = lpt_partition(cells, lambda c: c["device_s"], k)
-        loads = [sum(c["device_s"] for c in b) + sum(setup[m] for m in {c["model"] for c in b})
-                 for b in bins]
+        bins = lpt_partition(cells, lambda c: c["device_s"] + c["overhead_s"], k,
+                             group=lambda c: c["model"], setup=lambda m: start[m])
+        loads = [sum(c["device_s"] + c["overhead_s"] for c in b) +
+                 sum(start[m] for m in {c["model"] for c in b}) for b in bins]
         proj[str(k)] = round(max(loads), 3)
     out = Path(args.out)
     out.parent.mkdir(parents=True, exist_ok=True)
@@ -124,9 +129,9 @@ def main() -> int:
                "convert_s": round(convert_s, 3), "worker_prewarm_s": round(prewarm_s, 3),
                "per_model": per_model,
                "sweep_wall_s_projected_lpt": proj,
-               "projection": "LPT over measured per-cell device time + per-model worker "
-                             "start/graph capture (measured wall - device time), one worker "
-                             "per (model, GPU)",
+               "projection": "setup-aware LPT over measured per-cell device time + per-cell "
+                             "overhead (the model's measured wall - device time, split over its "
+                             "cells) + one worker start per (model, GPU hosting it)",
                "cells": cells}
     out.with_suffix(".json").write_text(json.dumps(summary, indent=1))
     print(json.dumps({k: summary[k] for k in ("sweep_wall_s_measured", "sweep_wall_s_projected_lpt",
