@@ -32,26 +32,31 @@ B2_DEV uint64_t smem_desc_mn_sw128(uint32_t addr) {
   return d;
 }
 
-// Persistent: one CTA per SM walks (sample, head) units; the next unit's
-// Q/K/V TMA load is issued into the other buffer before this unit's math, so
-// HBM latency overlaps compute.  8 warps: warps w and w + 4 share TMEM lane
-// quadrant w & 3 (query rows) and split the 128 keys (and the 64 output
-// columns) in halves; row max / sum are combined through shared memory.
+// Persistent, TWO CTAs per SM walking (sample, head) units: each unit is a
+// serial chain (S MMA -> softmax -> P -> PV MMA -> context), so a second
+// resident CTA fills the tensor pipe / issue slots while the first is in its
+// softmax or waiting on an MMA (one CTA per SM measured 39 us per BERT layer
+// at b=128, 2.6 TB/s).  The next unit's Q/K/V TMA load is issued into the
+// other buffer before this unit's math.  P (128 x 128 bf16) overwrites the
+// unit's Q|K region once S = QK^T has completed, which keeps a CTA at 99 KB.
+// 8 warps: warps w and w + 4 share TMEM lane quadrant w & 3 (query rows) and
+// split the 128 keys (and the 64 output columns) in halves; row max / sum are
+// combined through shared memory.
 constexpr int AT_WARPS = 8;
 constexpr int AT_QKV = 3 * 16384;
-constexpr int AT_SMEM = 2 * AT_QKV + 2 * 16384 + 4 * 128 * 4 + 1024 + 64;
+constexpr int AT_SMEM = 2 * AT_QKV + 4 * 128 * 4 + 1024 + 64;
+constexpr int AT_CTAS_PER_SM = 2;
 
 B2_DEV void at_bar() { asm volatile("bar.sync 1, %0;" ::"n"(AT_WARPS * 32) : "memory"); }
 
-__global__ void __launch_bounds__(AT_WARPS * 32, 1)
+__global__ void __launch_bounds__(AT_WARPS * 32, AT_CTAS_PER_SM)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, bf16* __restrict__ out, int H,
                    int units) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sQKV = smem;                       // 2 buffers x (Q | K | V), 16 KB each
-  uint8_t* sP = smem + 2 * AT_QKV;            // two 16 KB atoms: keys 0-63, 64-127
-  float* red = reinterpret_cast<float*>(sP + 2 * 16384);   // [2 stats][2 halves][128 rows]
+  float* red = reinterpret_cast<float*>(smem + 2 * AT_QKV);   // [2 stats][2 halves][128 rows]
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + 4 * 128);   // load[2], mma
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3);
 
@@ -93,6 +98,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32, 1)
     mbar_wait(&bars[buf], (it >> 1) & 1);
     tc_fence_after();
     uint8_t* sQ = sQKV + buf * AT_QKV;
+    uint8_t* sP = sQ;   // two 16 KB atoms (keys 0-63, 64-127) over Q | K, dead after S
     if (warp == 0) {   // S = Q K^T (M=128 queries, N=128 keys, K=64)
       const uint64_t dq = smem_desc_sw128(smem_u32(sQ));
       const uint64_t dk = smem_desc_sw128(smem_u32(sQ + 16384));
@@ -203,8 +209,9 @@ cudaError_t attention_tc(const CUtensorMap& tm_qkv, bf16* out, int B, int H, cud
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int units = B * H;
-  return launch_pdl(attn_tc_kernel, dim3(units < sms ? units : sms), dim3(AT_WARPS * 32), AT_SMEM,
-                    st, tm_qkv, out, H, units);
+  const int slots = AT_CTAS_PER_SM * sms;
+  return launch_pdl(attn_tc_kernel, dim3(units < slots ? units : slots), dim3(AT_WARPS * 32),
+                    AT_SMEM, st, tm_qkv, out, H, units);
 }
 
 }  // namespace b2
