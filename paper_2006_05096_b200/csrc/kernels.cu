@@ -446,16 +446,13 @@ __global__ void __launch_bounds__(256) dwconv3_strip_kernel(const T* __restrict_
 // splits into whole strips of 8 (or is short), else 4; stride 2 best at 2;
 // B2_DW_OWT / B2_DW_OWT2 override, 1 = the flat per-output kernel)
 static int dw_owt(int stride, int OW) {
-  static int v1 = [] {
-    const char* e = getenv("B2_DW_OWT");
-    return e ? atoi(e) : 0;
-  }();
-  if (stride == 1 && v1 == 0) return (OW % 8 == 0 || OW < 16) ? 8 : 4;
-  static int v2 = [] {
-    const char* e = getenv("B2_DW_OWT2");
-    return e ? atoi(e) : 2;
-  }();
-  return stride == 1 ? v1 : v2;
+  // read per launch (not cached): launches are captured into CUDA graphs, so
+  // this runs once per plan state, and tests switch widths within a process
+  const char* e = getenv(stride == 1 ? "B2_DW_OWT" : "B2_DW_OWT2");
+  const int v = e ? atoi(e) : 0;
+  if (v) return v;
+  if (stride == 1) return (OW % 8 == 0 || OW < 16) ? 8 : 4;
+  return 2;
 }
 
 template <typename T, int STRIDE, int OWT>

@@ -346,3 +346,44 @@ def test_fp32_3xtf32(gpu_required, monkeypatch, kind, args, batch, tf32):
     monkeypatch.setenv("B2_TF32", tf32)
     blob = linear_plan(*args) if kind == "linear" else conv_plan(*args)
     check_fp32(blob, batch)
+
+
+def dw_plan(H, W, C, stride, act, seed=0):
+    """One depthwise 3x3 conv (pad 1) on an [H, W, C] input."""
+    OH = (H + 2 - 3) // stride + 1
+    OW = (W + 2 - 3) // stride + 1
+    b = P.PlanBuilder("dw")
+    x = b.tensor(H, W, C)
+    b.in_elems = C * H * W
+    b.op_p(P.OP_INPUT, [x, C, H, W, C])
+    rng = np.random.default_rng(seed)
+    y = b.tensor(OH, OW, C)
+    w = rng.standard_normal((C, 3, 3)) / 3.0
+    bias = rng.standard_normal(C) * 0.1
+    b.op_p(P.OP_DWCONV, [x, y, b.weight(w), b.weight(bias), H, W, C, stride, 1, OH, OW, act, 3])
+    b.out_elems = b.tensors[y].elems
+    b.op_p(P.OP_OUTPUT, [1, y, 0])
+    return b.build(P.DT_FP32)
+
+
+@pytest.mark.parametrize("H,W,C,stride,act", [
+    (5, 5, 8, 1, 2), (13, 17, 24, 1, 1), (7, 7, 40, 1, 0), (9, 31, 16, 1, 2),
+    (13, 13, 24, 2, 2), (8, 15, 8, 2, 1), (112, 112, 32, 1, 2), (56, 56, 144, 2, 2),
+])
+@pytest.mark.parametrize("owt", ["0", "1", "2", "4", "8"])
+def test_dwconv_strip_edges(gpu_required, monkeypatch, H, W, C, stride, act, owt):
+    """Depthwise 3x3: the row-strip kernel at every strip width (ragged last
+    strips, rows narrower than one strip, image-edge zero fill) and the flat
+    kernel (B2_DW_OWT=1), bf16 layerwise and fp32 against the fp64 oracle."""
+    if owt != "0":
+        monkeypatch.setenv("B2_DW_OWT", owt)
+        monkeypatch.setenv("B2_DW_OWT2", owt)
+    blob = dw_plan(H, W, C, stride, act)
+    check(blob, 3)
+    pl = P.decode(blob)
+    x = plan_ref.make_inputs(pl, 3, 4)
+    plan = R.Plan(blob, P.DT_FP32)
+    try:
+        assert plan_ref.normwise_err(plan.predict(x), plan_ref.forward(blob, x)) <= 1e-5
+    finally:
+        plan.close()
