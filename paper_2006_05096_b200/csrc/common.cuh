@@ -364,6 +364,14 @@ B2_DEV void tma_load_2d_pair(void* smem_dst, const CUtensorMap* map, uint32_t ba
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
       : "memory");
 }
+B2_DEV void tma_load_4d_pair(void* smem_dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                             int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
 B2_DEV void tma_load_im2col_4d_pair(void* smem_dst, const CUtensorMap* map, uint32_t bar_cluster,
                                     int c, int w, int h, int n, uint16_t off_w, uint16_t off_h) {
   asm volatile(

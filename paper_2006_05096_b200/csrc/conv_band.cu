@@ -389,10 +389,251 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------ CTA pair
+// N = 64 convs with resident weights (ResNet layer1 3x3, VGG block 1) are
+// capped by the ISA at half the tensor rate with M = 128 (a 128x64x16 UMMA
+// takes as long as 128x128x16).  The pair form (cta_group::2, M = 256) at
+// N = 64 measured 43 cycles per MMA instead of 2 x 64: 1.48x the per-SM rate
+// (tools/umma_rate.cu).  Here the two CTAs of a cluster take bands u = 2p and
+// 2p + 1 of the same unit order: each loads its own band box and half of the
+// weight rows (32 of 64) into the same shared-memory offsets, the leader
+// issues M = 256 UMMAs whose rows 0-127 come from its band and 128-255 from
+// the peer's, and each CTA's epilogue drains its own TMEM lanes exactly as in
+// conv_band_kernel.  An odd unit count leaves the last peer without a band:
+// it re-loads the leader's band (the MMA needs both halves) and stores nothing.
+template <int ACT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CB_THREADS, 1)
+    conv_band_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                          const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ CUtensorMap tmO,
+                          const __grid_constant__ CUtensorMap tmO2, const BandArgs a) {
+  constexpr int BN = 64, RB = 128, R = 3, S = 3, TAPS = R * S, KSTEPS = 4;
+  constexpr int B_BLOCK = (BN / 2) * 128;     // this CTA's 32 weight rows of one K block
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + a.a_stages * a.a_stage_bytes;
+  uint8_t* sEpi = sB + a.kblocks * B_BLOCK;
+  uint64_t* afull = reinterpret_cast<uint64_t*>(sEpi + CB_EPI_BYTES);
+  uint64_t* aempty = afull + a.a_stages;
+  uint64_t* tfull = aempty + a.a_stages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bres = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
+
+  const int warp = warp_index_uniform();
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int units = a.B * a.nbands * a.nseg;
+  const int npairs = (units + 1) / 2;
+  auto mtv = [&](int u) {
+    const int seg = u % a.nseg;
+    const int band = (u / a.nseg) % a.nbands;
+    const int vr = min(a.bh, a.H - band * a.bh);
+    const int segw = seg < a.nseg - 1 ? a.seg_w : a.W - seg * a.seg_w;
+    return ((vr - 1) * a.Wp + segw - 1) / 128 + 1;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.a_stages; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * CB_EPI_WARPS);   // both CTAs' epilogue warps
+    }
+    mbar_init(bres, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmO);
+    tma_prefetch_desc(&tmO2);
+  }
+  cluster_sync();                       // barrier inits visible to the peer
+  if (warp == 1) tmem_alloc_pair(tmem_slot, a.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = uniform_u32(*tmem_slot);
+  pdl_wait();
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      const uint32_t bres_l = mapa_shared(bres, 0);
+      if (rank == 0) mbar_arrive_expect_tx(bres, (uint32_t)(2 * a.kblocks * B_BLOCK));
+      for (int kb = 0; kb < a.kblocks; ++kb)
+        tma_load_2d_pair(sB + kb * B_BLOCK, &tmB, bres_l, kb * 64, (int)rank * (BN / 2));
+      int as = 0;
+      uint32_t aph = 0;
+      for (int p = cid; p < npairs; p += ncl) {
+        int u = 2 * p + (int)rank;
+        if (u >= units) u = 2 * p;                  // no band for the peer: reload the leader's
+        const int seg = u % a.nseg;
+        const int band = (u / a.nseg) % a.nbands;
+        const int img = u / a.nseg / a.nbands;
+        mbar_wait(&aempty[as], aph ^ 1);
+        if (rank == 0) mbar_arrive_expect_tx(&afull[as], (uint32_t)(2 * a.a_box_bytes));
+        tma_load_4d_pair(sA + as * a.a_stage_bytes, &tmA, mapa_shared(&afull[as], 0), 0,
+                         seg * a.seg_w + a.x0, band * a.bh + a.y0, img);
+        if (++as == a.a_stages) {
+          as = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader, whole warp)
+    if (rank == 0) {
+      constexpr uint32_t idesc = make_idesc(256, BN, 1u);
+      uint32_t toff[TAPS];
+#pragma unroll
+      for (int t = 0; t < TAPS; ++t) toff[t] = (uint32_t)(((t / S) * a.Wp + (t % S)) * RB) >> 4;
+      constexpr uint32_t MT_STEP = (128 * RB) >> 4;
+      mbar_wait(bres, 0);
+      tc_fence_after();
+      const uint64_t bdesc0 = smem_desc_sw128(smem_u32(sB));
+      int as = 0;
+      uint32_t aph = 0;
+      int it = 0;
+      for (int p = cid; p < npairs; p += ncl, ++it) {
+        const int m0 = mtv(2 * p);
+        const int m1 = 2 * p + 1 < units ? mtv(2 * p + 1) : m0;
+        const int mt_valid = m0 > m1 ? m0 : m1;
+        const int ab = it & 1;
+        mbar_wait(&tempty[ab], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dbase = tmem_base + ab * a.MT * BN;
+        mbar_wait(&afull[as], aph);
+        tc_fence_after();
+        const uint64_t adesc0 = smem_desc_sw128(smem_u32(sA + as * a.a_stage_bytes));
+        for (int mt = 0; mt < mt_valid; ++mt) {
+          const uint64_t adm = adesc0 + mt * MT_STEP;
+#pragma unroll
+          for (int t = 0; t < TAPS; ++t) {
+#pragma unroll
+            for (int kk = 0; kk < KSTEPS; ++kk) {
+              const int kg = t * 64 + kk * 16;
+              const uint32_t boff = (uint32_t)((kg >> 6) * B_BLOCK + ((kg >> 4) & 3) * 32) >> 4;
+              if (elect_one())
+                umma_bf16_pair(dbase + mt * BN, adm + toff[t] + kk * 2, bdesc0 + boff, idesc,
+                               (t | kk) != 0 ? 1u : 0u);
+            }
+          }
+        }
+        if (elect_one()) umma_commit_pair(&aempty[as]);
+        if (++as == a.a_stages) {
+          as = 0;
+          aph ^= 1;
+        }
+        if (elect_one()) umma_commit_pair(&tfull[ab]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int q = warp & 3;
+    const int ew = warp - 2;
+    const int eh = ew >> 2;
+    uint8_t* obuf = sEpi + ew * 4096;
+    uint32_t oi = 0;
+    const uint32_t swz = (lane >> 1) & 3;
+    const uint32_t trem = rank == 0 ? 0u : mapa_shared(&tempty[0], 0);
+    float bpre[32];
+    {
+      const float4* bp = reinterpret_cast<const float4*>(a.bias + eh * 32);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 b4 = __ldg(bp + j);
+        bpre[4 * j] = b4.x;
+        bpre[4 * j + 1] = b4.y;
+        bpre[4 * j + 2] = b4.z;
+        bpre[4 * j + 3] = b4.w;
+      }
+    }
+    int it = 0;
+    for (int p = cid; p < npairs; p += ncl, ++it) {
+      const int u = 2 * p + (int)rank;
+      const int ab = it & 1;
+      mbar_wait(&tfull[ab], (it >> 1) & 1);
+      tc_fence_after();
+      if (u < units) {
+        const int seg = u % a.nseg;
+        const int band = (u / a.nseg) % a.nbands;
+        const int img = u / a.nseg / a.nbands;
+        const int vr = min(a.bh, a.H - band * a.bh);
+        const int mt_valid = mtv(u);
+        const CUtensorMap* omap = seg == 0 ? &tmO : &tmO2;
+        for (int mt = 0; mt < mt_valid; ++mt) {
+          const int p0 = mt * 128 + q * 32;
+          const uint32_t taddr =
+              tmem_base + ((uint32_t)(q * 32) << 16) + ab * a.MT * BN + mt * BN + eh * 32;
+          uint32_t rr[32];
+          tmem_ld_32x32b_x32(taddr, rr);
+          tmem_wait_ld();
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          uint8_t* orow = obuf + (oi & 1) * 2048 + lane * 64;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              v[e] = act_t<ACT>(__uint_as_float(rr[8 * j + e]) + bpre[8 * j + e]);
+            uint4 w;
+            w.x = pack_bf16x2(v[0], v[1]);
+            w.y = pack_bf16x2(v[2], v[3]);
+            w.z = pack_bf16x2(v[4], v[5]);
+            w.w = pack_bf16x2(v[6], v[7]);
+            *reinterpret_cast<uint4*>(orow + ((j ^ swz) << 4)) = w;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const uint8_t* src = obuf + (oi & 1) * 2048;
+            if (a.Wp >= 32) {
+              const int r = p0 / a.Wp;
+              if (r < vr) tma_store_4d(omap, src, eh * 32, p0 - r * a.Wp, band * a.bh + r, img);
+            } else {
+              for (int j = 0; j < 32 / a.Wp; ++j) {
+                const int r = p0 / a.Wp + j;
+                if (r < vr) tma_store_4d(omap, src + j * a.Wp * 64, eh * 32, 0, band * a.bh + r, img);
+              }
+            }
+            bulk_commit();
+          }
+          ++oi;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (rank == 0) mbar_arrive(&tempty[ab]);
+        else mbar_arrive_cluster(trem + ab * 8);
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();                       // the peer's remote arrivals / the leader's MMAs are done
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, a.tmem_cols);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 
 int band_smem_bytes(const BandArgs& a, int bn) {
   const int nb = a.b_resident ? a.kblocks : a.b_stages;
+  if (a.pair) bn /= 2;   // each CTA of a pair holds half the weight rows
   return 1024 + a.a_stages * a.a_stage_bytes + nb * bn * 128 + CB_EPI_BYTES +
          8 * (2 * a.a_stages + 2 * a.b_stages + 5) + 16;
 }
@@ -489,6 +730,24 @@ static cudaError_t band_launch_t(const BandArgs& a, const CUtensorMap& ta, const
 }
 
 template <int ACT>
+static cudaError_t band_pair_launch_t(const BandArgs& a, const CUtensorMap& ta,
+                                      const CUtensorMap& tb, const CUtensorMap& to,
+                                      const CUtensorMap& to2, int num_sms, cudaStream_t st) {
+  auto kern = conv_band_pair_kernel<ACT>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         CB_SMEM_MAX);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int npairs = (a.B * a.nbands * a.nseg + 1) / 2;
+  const int pairs = npairs < num_sms / 2 ? npairs : num_sms / 2;
+  return launch_pdl(kern, dim3(2 * pairs), dim3(CB_THREADS), band_smem_bytes(a, 64), st, ta, tb,
+                    to, to2, a);
+}
+
+template <int ACT>
 static cudaError_t band_dispatch(const BandArgs& a, int bn, int cgw, const CUtensorMap& ta,
                                  const CUtensorMap& tb, const CUtensorMap& to,
                                  const CUtensorMap& to2, int num_sms, cudaStream_t st) {
@@ -505,6 +764,11 @@ static cudaError_t band_dispatch(const BandArgs& a, int bn, int cgw, const CUten
     return cudaErrorInvalidValue;
   }
   if (a.R != 3 || a.S != 3) return cudaErrorInvalidValue;
+  if (a.pair) {
+    if (bn == 64 && a.CG == 1 && a.b_resident && a.tiles_n == 1)
+      return band_pair_launch_t<ACT>(a, ta, tb, to, to2, num_sms, st);
+    return cudaErrorInvalidValue;
+  }
   if (a.b_resident) {
     if (bn == 64 && a.CG == 1) return band_launch_t<64, 64, 3, 3, true, ACT>(a, ta, tb, to, to2, num_sms, st);
     return cudaErrorInvalidValue;

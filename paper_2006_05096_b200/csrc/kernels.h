@@ -64,6 +64,7 @@ struct BandArgs {
   // geometry chosen by band_config
   int bh, nbands, MT;
   int a_box_bytes, a_stage_bytes, a_stages, b_stages, b_resident, tmem_cols;
+  int pair;             // CTA-pair kernel (N = 64, resident weights): M = 256 UMMAs over two bands
   const float* bias;
   bf16* out;
   int act;
@@ -73,6 +74,7 @@ struct BandArgs {
 };
 bool band_config(BandArgs& a, int bn, int cgw, int mt_cap = 4);
 bool band_supported(const BandArgs& a, int bn, int cgw, int act);
+int band_smem_bytes(const BandArgs& a, int bn);
 bool stem_pool_config(BandArgs& a);
 cudaError_t stem_pool_launch(const BandArgs& a, const CUtensorMap& ta, const CUtensorMap& tb,
                              int num_sms, cudaStream_t st);

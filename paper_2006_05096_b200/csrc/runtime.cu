@@ -293,6 +293,7 @@ struct b2_plan {
                              // (correct, but issue-bound on 2 KB boxes: slower than gather)
   bool use_band = true;      // B2_BAND=0 -> stride-1 k x k convs and s2d stems on gemm_tc
   bool use_pair = true;      // B2_PAIR=0 -> single-CTA tc_gemm only
+  bool band_pair = true;     // B2_BAND_PAIR=0 -> single-CTA band kernel for N = 64
   bool verbose = false;      // B2_VERBOSE=1: per-layer kernel choices on stderr
   long pair_min_m = 4096;    // B2_PAIR_MIN_M: smallest M sent to the CTA-pair GEMM
   int pair_min_k = 0;        // B2_PAIR_MIN_K: shortest K sent to the CTA-pair GEMM
@@ -1110,6 +1111,17 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
     BandArgs t = a;
     if (band_config(t, bn, cgw, 1) && band_supported(t, bn, cgw, t.act)) a = t;
   }
+  // CTA pair (M = 256 UMMAs over two bands): N = 64 with resident weights,
+  // when there are enough bands to give every pair of SMs work.  Measured:
+  // ResNet layer1 3x3 b=256 69 -> 66 us; VGG 224x224 (two column segments per
+  // row) 1.05 -> 1.34 ms, so single-segment rows only
+  if (pl->band_pair && cgw == 64 && bn == 64 && a.CG == 1 && a.b_resident && a.tiles_n == 1 &&
+      a.R == 3 && a.S == 3 && L.pool_op < 0 && a.nseg == 1 &&
+      (long)a.B * a.nbands * a.nseg >= pl->num_sms) {
+    BandArgs t = a;
+    t.pair = 1;
+    if (band_smem_bytes(t, 64) <= 232448) a = t;
+  }
   EncodeTiledFn fn = encode_fn();
   if (!fn) return -fail(B2_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const int cin = L.s2d ? 16 : C;
@@ -1128,7 +1140,7 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -fail(B2_ERR_CUDA, "layer %zu: band A tensor map rejected", li);
   if (!make_tmap_bf16(&S.tmB[li], L.w, (uint64_t)N, (uint64_t)L.kpad, (uint64_t)L.kpad * 2,
-                      (uint32_t)bn))
+                      (uint32_t)(a.pair ? bn / 2 : bn)))
     return -fail(B2_ERR_CUDA, "layer %zu: band B tensor map rejected", li);
   // output NHWC [B, OH, OW, N]: 32-channel x 32-pixel boxes, 64 B swizzle;
   // one map per column segment, each clipping at its own width
@@ -1443,6 +1455,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* sd = getenv("B2_S2D")) pl->use_s2d = sd[0] != '0';
   if (const char* bd = getenv("B2_BAND")) pl->use_band = bd[0] != '0';
   if (const char* pr = getenv("B2_PAIR")) pl->use_pair = pr[0] != '0';
+  if (const char* bp = getenv("B2_BAND_PAIR")) pl->band_pair = bp[0] != '0';
   if (const char* vb = getenv("B2_VERBOSE")) pl->verbose = vb[0] == '1';
   if (const char* pm = getenv("B2_PAIR_MIN_M")) pl->pair_min_m = atol(pm);
   if (const char* pk = getenv("B2_PAIR_MIN_K")) pl->pair_min_k = atoi(pk);

@@ -387,3 +387,17 @@ def test_dwconv_strip_edges(gpu_required, monkeypatch, H, W, C, stride, act, owt
         assert plan_ref.normwise_err(plan.predict(x), plan_ref.forward(blob, x)) <= 1e-5
     finally:
         plan.close()
+
+
+@pytest.mark.parametrize("H,W,batch", [
+    (56, 56, 48),    # ResNet layer1 3x3: 336 bands, CTA pairs
+    (56, 56, 23),    # odd band count: the last pair's peer has no band
+    (224, 224, 3),   # VGG block 1: two column segments per row
+    (30, 44, 40),    # ragged: partial last band, W not a multiple of the pitch
+])
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_band_pair(gpu_required, monkeypatch, H, W, batch, pair):
+    """N = 64 3x3 convs on the CTA-pair band kernel (M = 256 UMMAs over two
+    bands, each CTA holding half of the resident weights) and the single-CTA one."""
+    monkeypatch.setenv("B2_BAND_PAIR", pair)
+    check(conv_plan(H, W, 64, 64, 3, 1), batch)
