@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import os
 import signal
 import socketserver
 import sys
@@ -243,7 +244,11 @@ def main(argv=None) -> int:
         print(f"no usable device: {exc}", file=sys.stderr)
         return NO_DEVICE_EXIT
     server = serve(ex, args.protocol, args.host)
-    signal.signal(signal.SIGTERM, lambda *_: sys.exit(0))
+    # SIGTERM ends the process at once: the driver reclaims the CUDA context
+    # and device memory.  A graceful interpreter shutdown (module teardown,
+    # context destroy) took 2-3 s per worker, which the profiler's per-job
+    # instance teardown (run_sweep) waited for between models.
+    signal.signal(signal.SIGTERM, lambda *_: os._exit(0))
     print(f"READY {server.server_address[1]}", flush=True)
     try:
         server.serve_forever(poll_interval=0.05)
