@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <chrono>
 #include <stdlib.h>
 #include <string.h>
 
@@ -1466,6 +1467,9 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* sk = getenv("B2_SPLIT")) pl->use_split = sk[0] != '0';
   if (const char* cz = getenv("B2_CHAIN")) pl->use_chain = cz[0] != '0';
   if (const char* bm = getenv("B2_BAND_MAX_N")) pl->band_max_n = atoi(bm);
+  const auto tv0 = std::chrono::steady_clock::now();
+  cudaFree(nullptr);   // context creation, timed separately under B2_VERBOSE
+  const auto tv1 = std::chrono::steady_clock::now();
   cudaGetDevice(&pl->device);
   cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, pl->device);
   int major = 0;
@@ -1509,6 +1513,13 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
       std::vector<float> z(8192, 0.f);
       rc = upload_f32(pl, z.data(), z.size(), &pl->zero_bias);
     }
+  }
+  if (pl->verbose) {
+    cudaDeviceSynchronize();
+    const auto tv2 = std::chrono::steady_clock::now();
+    fprintf(stderr, "b2: plan create: context %.3f s, weights %.3f s (%zu bytes of blob)\n",
+            std::chrono::duration<double>(tv1 - tv0).count(),
+            std::chrono::duration<double>(tv2 - tv1).count(), len);
   }
   if (pl->stage) {
     if (cudaDeviceSynchronize() != cudaSuccess && !rc) rc = fail(B2_ERR_CUDA, "weight upload failed");

@@ -227,7 +227,9 @@ def encode(plan: Plan) -> bytes:
     return bytes(out) + struct.pack("<I", zlib.crc32(out))
 
 
-def decode(blob: bytes) -> Plan:
+def decode(blob: bytes, verify_crc: bool = True) -> Plan:
+    """Parse a plan.  ``verify_crc=False`` skips the whole-blob CRC for callers
+    that hand the bytes to ``b2_plan_create`` next (it verifies them again)."""
     if len(blob) < _HDR.size + 4:
         raise PlanFormatError("truncated plan")
     (magic, version, dtype, nt, nw, no, in_kind, in_elems, out_elems, meta_len, _r0,
@@ -236,7 +238,7 @@ def decode(blob: bytes) -> Plan:
         raise PlanFormatError("bad magic, not a b200-plan")
     if version != VERSION:
         raise PlanFormatError(f"unsupported plan version {version}")
-    if zlib.crc32(memoryview(blob)[:-4]) != struct.unpack("<I", blob[-4:])[0]:
+    if verify_crc and zlib.crc32(memoryview(blob)[:-4]) != struct.unpack("<I", blob[-4:])[0]:
         raise PlanFormatError("CRC mismatch, plan corrupted")
     pos = _HDR.size
     need = pos + nt * _TEN.size + nw * _WGT.size + no * _OP.size + meta_len
