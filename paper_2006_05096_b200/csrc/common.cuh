@@ -40,6 +40,54 @@ B2_DEV float gelu_erf(float v) {
   return 0.5f * v * (1.f + copysignf(1.f - r, v));
 }
 
+// Two GELUs on packed fp32 pairs (Blackwell FFMA2 / FMUL2 via fma.rn.f32x2 /
+// mul.rn.f32x2): the same A&S 7.1.28 arithmetic as gelu_erf, per-lane
+// identical results (f32x2 ops round each lane exactly like the scalar op),
+// at about half the issue slots -- the BERT FFN GEMM epilogue is issue-bound.
+B2_DEV uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+B2_DEV void f2unpack(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+B2_DEV uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+B2_DEV uint64_t f2mul(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+B2_DEV void gelu_erf2(float& va, float& vb) {
+  const float c = 0.70710678118654752f;
+  const uint64_t z = f2pack(fabsf(va) * c, fabsf(vb) * c);
+  uint64_t p = f2fma(z, f2pack(0.0000430638f, 0.0000430638f), f2pack(0.0002765672f, 0.0002765672f));
+  p = f2fma(z, p, f2pack(0.0001520143f, 0.0001520143f));
+  p = f2fma(z, p, f2pack(0.0092705272f, 0.0092705272f));
+  p = f2fma(z, p, f2pack(0.0422820123f, 0.0422820123f));
+  p = f2fma(z, p, f2pack(0.0705230784f, 0.0705230784f));
+  p = f2fma(z, p, f2pack(1.f, 1.f));
+  float pa, pb;
+  f2unpack(p, pa, pb);
+  uint64_t r = f2pack(__fdividef(1.f, pa), __fdividef(1.f, pb));
+  r = f2mul(r, r);
+  r = f2mul(r, r);
+  r = f2mul(r, r);
+  r = f2mul(r, r);
+  float ra, rb;
+  f2unpack(r, ra, rb);
+  const float ea = copysignf(1.f - ra, va), eb = copysignf(1.f - rb, vb);
+  const uint64_t h = f2mul(f2pack(va, vb), f2pack(0.5f, 0.5f));
+  float oa, ob;
+  f2unpack(f2fma(h, f2pack(ea, eb), h), oa, ob);
+  va = oa;
+  vb = ob;
+}
+
 B2_DEV float act_apply(float v, int act) {
   switch (act) {
     case ACT_RELU: return fmaxf(v, 0.f);

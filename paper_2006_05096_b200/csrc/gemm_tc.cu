@@ -158,6 +158,12 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint
 #pragma unroll
         for (int q = 0; q < 4; ++q) add_bf16x8(v + 8 * q, rcur[q]);
       }
+      // GELU on packed pairs (f32x2 FMAs); other activations per element below
+      constexpr int PACT = ACT == ACT_GELU ? ACT_NONE : ACT;
+      if constexpr (ACT == ACT_GELU) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) gelu_erf2(v[2 * j], v[2 * j + 1]);
+      }
       if (lane == 0 && a.epi_debug != 4 && a.epi_debug != 5) bulk_wait_read<1>();
       __syncwarp();
       uint8_t* sbuf = obuf + (oi & 1) * 2048;
@@ -169,10 +175,10 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint
           continue;
         }
         uint4 u;
-        u.x = pack_bf16x2(act_t<ACT>(v[q * 8 + 0]), act_t<ACT>(v[q * 8 + 1]));
-        u.y = pack_bf16x2(act_t<ACT>(v[q * 8 + 2]), act_t<ACT>(v[q * 8 + 3]));
-        u.z = pack_bf16x2(act_t<ACT>(v[q * 8 + 4]), act_t<ACT>(v[q * 8 + 5]));
-        u.w = pack_bf16x2(act_t<ACT>(v[q * 8 + 6]), act_t<ACT>(v[q * 8 + 7]));
+        u.x = pack_bf16x2(act_t<PACT>(v[q * 8 + 0]), act_t<PACT>(v[q * 8 + 1]));
+        u.y = pack_bf16x2(act_t<PACT>(v[q * 8 + 2]), act_t<PACT>(v[q * 8 + 3]));
+        u.z = pack_bf16x2(act_t<PACT>(v[q * 8 + 4]), act_t<PACT>(v[q * 8 + 5]));
+        u.w = pack_bf16x2(act_t<PACT>(v[q * 8 + 6]), act_t<PACT>(v[q * 8 + 7]));
         *reinterpret_cast<uint4*>(orow + ((q ^ swz) << 4)) = u;
       }
       if (a.epi_debug != 3) fence_proxy_async_smem();
