@@ -64,6 +64,23 @@ B2_DEV void add_bf16x8(float* v, const uint4& u) {
 
 // TMA-store epilogue of one warp, specialised on the activation so the
 // per-element math is branch-free.
+// B2_GEMM_TS=2: per-tile stamps of CTA 0's first 32 tiles (globaltimer, ns):
+// [0] producer past empty-wait, [1] MMA past full-wait, [2] MMA commits issued,
+// [3] epilogue warp 2 past tfull-wait, [4] epilogue warp 2 arrived tempty
+__device__ unsigned long long g_tile_ts[5][32];
+// Compiled in only with -DB2_TILE_TS: the lane-0 branches inside the MMA issue
+// loop cost ~7% on single-K-block GEMMs (they break the converged issuer).
+B2_DEV void tile_stamp(const TcArgs& a, int which, int tile) {
+#ifndef B2_TILE_TS
+  return;
+#endif
+  if (a.ts_debug == 2 && blockIdx.x == 0 && tile < 32) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    g_tile_ts[which][tile] = g;
+  }
+}
+
 B2_DEV void split_range(int s, int nsplit, int KT, int& kb0, int& kb1) {
   kb0 = (int)((long)s * KT / nsplit);
   kb1 = (int)((long)(s + 1) * KT / nsplit);
@@ -120,6 +137,9 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint
     }
     mbar_wait(&tfull[as], aph);
     tc_fence_after();
+#ifdef B2_TILE_TS
+    if (ew == 0 && lane == 0) tile_stamp(a, 3, it);
+#endif
     const uint32_t taddr = tmem_base + (uint32_t(lg * 32) << 16) + as * BN;
 #pragma unroll 1
     for (int c = eh * 32; c < BN && n0 + c < a.N; c += 64) {   // ragged N: skip empty chunks
@@ -197,6 +217,9 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint
     if (lane == 0) {
       if (tempty_remote) mbar_arrive_cluster(tempty_remote + as * 8);
       else mbar_arrive(&tempty[as]);
+#ifdef B2_TILE_TS
+      if (ew == 0) tile_stamp(a, 4, it);
+#endif
     }
   }
   if (lane == 0) bulk_wait<0>();
@@ -293,6 +316,9 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
         }
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+#ifdef B2_TILE_TS
+          if (kb == kb0 && a.ts_debug == 2) tile_stamp(a, 0, (u - (int)blockIdx.x) / (int)gridDim.x);
+#endif
           if (kb >= a.kblocks) {
             const int j = kb - a.kblocks;
             mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
@@ -378,6 +404,9 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (it == 0 && kb == 0 && lane == 0) stamp(2);
+#ifdef B2_TILE_TS
+          if (kb == kb0 && lane == 0) tile_stamp(a, 1, it);
+#endif
           const bool tap8 = a.a_im2col == 2 && kb < a.kblocks;
           const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
           const uint64_t ad = tap8 ? smem_desc_kmajor_noswizzle(a_addr, 2048, 128)
@@ -395,6 +424,9 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
           }
         }
         if (elect_one()) umma_commit(&tfull[as]);
+#ifdef B2_TILE_TS
+        if (lane == 0) tile_stamp(a, 2, it);
+#endif
       }
       if (lane == 0) stamp(3);
     }
@@ -624,6 +656,14 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     printf("b2ts %d %u %llu %llu %llu %llu %llu %llu\n", blockIdx.x, smid, ts[0], ts[1], ts[2],
            ts[3], ts[4], ts[5]);
+#ifdef B2_TILE_TS
+    if (a.ts_debug == 2 && blockIdx.x == 0)
+#else
+    if (false)
+#endif
+      for (int t = 0; t < 32; ++t)
+        printf("b2tile %d %llu %llu %llu %llu %llu\n", t, g_tile_ts[0][t], g_tile_ts[1][t],
+               g_tile_ts[2][t], g_tile_ts[3][t], g_tile_ts[4][t]);
   }
   if (warp == 1) {
     tc_fence_after();
