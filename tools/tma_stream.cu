@@ -9,12 +9,15 @@
 #include "common.cuh"
 
 __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ CUtensorMap tm,
-                                                       int tiles, int box_rows, int stages) {
+                                                       const __grid_constant__ CUtensorMap tw,
+                                                       int tiles, int box_rows, int stages,
+                                                       int wbox) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const int box_bytes = box_rows * 128;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * box_bytes);
+  const int stage_bytes = box_bytes + wbox * 128;   // + an L2-resident "weights" box
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
   uint64_t* empty = full + stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -30,8 +33,9 @@ __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ C
     uint32_t ph = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       mbar_wait(&empty[st], ph ^ 1);
-      mbar_arrive_expect_tx(&full[st], box_bytes);
-      tma_load_2d(smem + st * box_bytes, &tm, &full[st], 0, t * box_rows);
+      mbar_arrive_expect_tx(&full[st], stage_bytes);
+      tma_load_2d(smem + st * stage_bytes, &tm, &full[st], 0, t * box_rows);
+      if (wbox) tma_load_2d(smem + st * stage_bytes + box_bytes, &tw, &full[st], 0, 0);
       if (++st == stages) { st = 0; ph ^= 1; }
     }
   } else if (warp == 1 && lane == 0) {
@@ -66,8 +70,21 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int box_rows : {64, 128, 256}) {
-    CUtensorMap tm;
+  void* wbuf;
+  cudaMalloc(&wbuf, 1 << 20);
+  cudaMemset(wbuf, 1, 1 << 20);
+  for (int wbox : {0, 32, 64})
+  for (int box_rows : {128}) {
+    CUtensorMap tm, tw;
+    {
+      cuuint64_t wd[2] = {64, 4096};
+      cuuint64_t wst[1] = {128};
+      cuuint32_t wb[2] = {64, (cuuint32_t)(wbox ? wbox : 32)};
+      cuuint32_t wes[2] = {1, 1};
+      enc(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, wbuf, wd, wst, wb, wes,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     cuuint64_t dims[2] = {64, rows};
     cuuint64_t str[1] = {128};
     cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
@@ -76,17 +93,17 @@ int main() {
         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     const int tiles = (int)(rows / box_rows);
-    for (int stages : {2, 4, 8, 12}) {
-      const int smem = stages * box_rows * 128 + 2048;
+    for (int stages : {2, 4, 8}) {
+      const int smem = stages * (box_rows + wbox) * 128 + 2048;
       if (smem > 232448) continue;
-      stream_kernel<<<sms, 64, smem>>>(tm, tiles, box_rows, stages);
+      stream_kernel<<<sms, 64, smem>>>(tm, tw, tiles, box_rows, stages, wbox);
       cudaEventRecord(e0);
-      for (int r = 0; r < 5; ++r) stream_kernel<<<sms, 64, smem>>>(tm, tiles, box_rows, stages);
+      for (int r = 0; r < 5; ++r) stream_kernel<<<sms, 64, smem>>>(tm, tw, tiles, box_rows, stages, wbox);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms = 0;
       cudaEventElapsedTime(&ms, e0, e1);
-      printf("box %3d rows (%3d KB) stages %2d (%4d KB in flight/SM): %7.1f GB/s  (%s)\n", box_rows,
+      printf("wbox %2d  box %3d rows (%3d KB) stages %2d (%4d KB in flight/SM): %7.1f GB/s  (%s)\n", wbox, box_rows,
              box_rows * 128 / 1024, stages, stages * box_rows * 128 / 1024,
              5.0 * bytes / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
     }
