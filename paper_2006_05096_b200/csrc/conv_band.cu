@@ -71,7 +71,7 @@ B2_DEV uint64_t band_adesc(uint32_t addr) {
 // keep up with 64-cycle (N <= 128) / 128-cycle (N = 256) MMAs, and a loop with
 // runtime tap decomposition (integer division, parameter reloads) measured
 // ~170 cycles per MMA — the tensor pipe then idles 80% of the time.
-template <int BN, int CGW, int R, int S, bool BRES, int ACT>
+template <int BN, int CGW, int R, int S, bool BRES, int ACT, bool POOL = false>
 __global__ void __launch_bounds__(CB_THREADS, 1)
     conv_band_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB,
@@ -313,6 +313,73 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
       }
       mbar_wait(&tfull[ab], (it >> 1) & 1);
       tc_fence_after();
+      if constexpr (POOL) {
+        // fused 2x2/2 max-pool (Wp == 128: M tile mt = band row mt; bh even):
+        // rows 2j, 2j+1 meet in registers, column pairs across lanes 2i, 2i+1;
+        // even lanes stage 16 pooled pixels x 32 channels, one TMA store
+        const int segw0 = seg < a.nseg - 1 ? a.seg_w : a.W - seg * a.seg_w;
+        for (int mt = 0; mt + 1 < mt_valid; mt += 2) {
+          const int r = mt;                              // band row of the pair's top
+          if (r + 1 >= vr) break;
+          const int p0 = q * 32;                         // column of lane 0 in the segment
+#pragma unroll 1
+          for (int c = eh * 32; c < BN && n0 + c < a.N; c += 64) {
+            uint32_t ra[32], rb[32];
+            const uint32_t tbase_mt =
+                tmem_base + ((uint32_t)(q * 32) << 16) + ab * a.MT * BN + c;
+            tmem_ld_32x32b_x32(tbase_mt + mt * BN, ra);
+            tmem_ld_32x32b_x32(tbase_mt + (mt + 1) * BN, rb);
+            float bv[32];
+            if constexpr (BN == 64) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) bv[j] = bpre[j];
+            } else {
+              const float4* bp = reinterpret_cast<const float4*>(a.bias + n0 + c);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 b4 = __ldg(bp + j);
+                bv[4 * j] = b4.x;
+                bv[4 * j + 1] = b4.y;
+                bv[4 * j + 2] = b4.z;
+                bv[4 * j + 3] = b4.w;
+              }
+            }
+            tmem_wait_ld();
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float x0 = act_t<ACT>(__uint_as_float(ra[j]) + bv[j]);
+              const float x1 = act_t<ACT>(__uint_as_float(rb[j]) + bv[j]);
+              const float m = fmaxf(x0, x1);
+              v[j] = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+            }
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            uint8_t* sbuf = obuf + (oi & 1) * 2048;
+            if ((lane & 1) == 0) {
+              // 16 rows x 64 B, 64B-swizzled like the unpooled staging tile
+              const int prow = lane >> 1;
+              const uint32_t pswz = (prow >> 1) & 3;
+              uint8_t* orow = sbuf + prow * 64;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                uint4 w;
+                w.x = pack_bf16x2(v[8 * j + 0], v[8 * j + 1]);
+                w.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
+                w.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
+                w.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
+                *reinterpret_cast<uint4*>(orow + ((j ^ pswz) << 4)) = w;
+              }
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && p0 < segw0)
+              tma_store_4d(omap, sbuf, n0 + c, p0 >> 1, (band * a.bh + r) >> 1, img);
+            if (lane == 0) bulk_commit();
+            ++oi;
+          }
+        }
+      } else
       for (int mt = 0; mt < mt_valid; ++mt) {
         const int p0 = mt * 128 + q * 32;               // band position of lane 0
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + ab * a.MT * BN + mt * BN;
@@ -667,6 +734,7 @@ bool band_config(BandArgs& a, int bn, int cgw, int mt_cap) {
     int bh = (mt * 128) / a.Wp;
     if (bh < 1) continue;
     if (bh > a.H) bh = a.H;
+    if (a.pool2 && (bh & 1)) continue;   // fused 2x2 pool: whole row pairs per band
     const int bands = (a.H + bh - 1) / bh;
     double computed = 0.0;
     for (int b = 0; b < bands; ++b) {
@@ -680,7 +748,9 @@ bool band_config(BandArgs& a, int bn, int cgw, int mt_cap) {
     t.b_resident = 1;
     t.b_stages = 0;
     t.a_stages = 2;
-    const bool res_ok = a.tiles_n == 1 && a.CG == 1 && bn == 64;   // instantiated resident kernels
+    // instantiated resident kernels (the pooling epilogue streams its weights:
+    // resident 3x3x64x64 leaves room only for one-row bands)
+    const bool res_ok = a.tiles_n == 1 && a.CG == 1 && bn == 64 && !a.pool2;
     (void)0;
     if (res_ok && band_smem_bytes(t, bn) <= CB_SMEM_MAX) {
       c.res = 1;
@@ -711,11 +781,11 @@ bool band_config(BandArgs& a, int bn, int cgw, int mt_cap) {
   return band_smem_bytes(a, bn) <= CB_SMEM_MAX;
 }
 
-template <int BN, int CGW, int R, int S, bool BRES, int ACT>
+template <int BN, int CGW, int R, int S, bool BRES, int ACT, bool POOL = false>
 static cudaError_t band_launch_t(const BandArgs& a, const CUtensorMap& ta, const CUtensorMap& tb,
                                  const CUtensorMap& to, const CUtensorMap& to2, int num_sms,
                                  cudaStream_t st) {
-  auto kern = conv_band_kernel<BN, CGW, R, S, BRES, ACT>;
+  auto kern = conv_band_kernel<BN, CGW, R, S, BRES, ACT, POOL>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -767,6 +837,13 @@ static cudaError_t band_dispatch(const BandArgs& a, int bn, int cgw, const CUten
   if (a.pair) {
     if (bn == 64 && a.CG == 1 && a.b_resident && a.tiles_n == 1)
       return band_pair_launch_t<ACT>(a, ta, tb, to, to2, num_sms, st);
+    return cudaErrorInvalidValue;
+  }
+  if (a.pool2) {   // fused 2x2 max-pool (VGG): ReLU only (checked on the host)
+    if constexpr (ACT == ACT_RELU) {
+      if (bn == 128 && !a.b_resident)
+        return band_launch_t<128, 64, 3, 3, false, ACT_RELU, true>(a, ta, tb, to, to2, num_sms, st);
+    }
     return cudaErrorInvalidValue;
   }
   if (a.b_resident) {

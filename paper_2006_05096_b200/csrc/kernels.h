@@ -65,6 +65,7 @@ struct BandArgs {
   int bh, nbands, MT;
   int a_box_bytes, a_stage_bytes, a_stages, b_stages, b_resident, tmem_cols;
   int pair;             // CTA-pair kernel (N = 64, resident weights): M = 256 UMMAs over two bands
+  int pool2;            // fused 2x2/2 max-pool epilogue (Wp == 128: one output row per M tile)
   const float* bias;
   bf16* out;
   int act;

@@ -223,6 +223,7 @@ struct Layer {
   int s2d_shift = 0, s2d_H2 = 0, s2d_W2 = 0, s2d_Rp = 0, s2d_creal = 0;
   int im2col_mode = 0;      // TcArgs::a_im2col
   int pool_op = -1;         // s2d stem: index of the 3x3/s2 max-pool fused into its epilogue
+  int pool2_op = -1;        // band conv: index of the 2x2/s2 max-pool fused into its epilogue
   int ds_op = -1;           // 1x1 conv: index of the projection shortcut folded into its K loop
   int chain_op = -1;        // block-tail 1x1 conv: next block's 1x1 conv computed in the same kernel
   bool tf32 = false;        // fp32 plan conv/linear on the 3xTF32 tcgen05 GEMM (w = hi, w2 = lo)
@@ -429,6 +430,45 @@ void plan_fuse_pool(b2_plan* pl) {
         q[8] * 2 != q[2] || q[9] * 2 != q[3])
       continue;
     Lc.pool_op = pool;
+    pl->layers[pool].fused = true;
+    pl->virt[t] = 1;
+  }
+  // 3x3/1 band convs (VGG) followed by a 2x2/2 max-pool that is their only
+  // consumer: the band epilogue pools row pairs / column pairs and writes only
+  // the pooled tensor (needs one output row per M tile: band pitch 128).
+  // N = 128 only (streamed weights either way; measured VGG conv2_2 + pool2
+  // 0.811 + 0.237 -> 0.795 ms).  At N = 64 the even band height forces the
+  // weights out of shared memory: conv1_2 1.06 -> 1.64 ms, more than pool1's
+  // 0.46 ms saved.
+  for (size_t ci = 0; ci < pl->layers.size() && pl->dtype == B2_DT_BF16; ++ci) {
+    Layer& Lc = pl->layers[ci];
+    const int* p = Lc.p;
+    if (Lc.kind != OP_CONV || Lc.s2d || Lc.pool_op >= 0 || p[14] != ACT_RELU || p[15] >= 0 ||
+        p[8] != 3 || p[9] != 3 || p[10] != 1 || p[11] != 1 || p[6] % 64 != 0 ||
+        p[7] != 128 || p[7] > pl->band_max_n || p[12] != p[4] ||
+        p[13] != p[5] || (p[12] & 1) || (p[13] & 1) || p[13] + 2 <= 96 || p[13] > 2 * 126)
+      continue;
+    const int t = p[1];
+    int pool = -1, users = 0;
+    for (size_t j = 0; j < pl->layers.size(); ++j) {
+      const Layer& Lj = pl->layers[j];
+      if (j == ci) continue;
+      bool uses = false;
+      if (Lj.kind == OP_OUTPUT) {
+        for (int q = 0; q < Lj.p[0]; ++q) uses |= Lj.p[1 + 2 * q] == t;
+      } else if (Lj.kind != OP_INPUT && Lj.kind != OP_TOKENS) {
+        uses = Lj.p[0] == t || (Lj.kind == OP_CONV && Lj.p[15] == t) ||
+               (Lj.kind == OP_LINEAR && Lj.p[8] == t) || (Lj.kind == OP_LAYERNORM && Lj.p[7] == t);
+      }
+      if (uses) {
+        ++users;
+        if (Lj.kind == OP_MAXPOOL && Lj.p[0] == t) pool = (int)j;
+      }
+    }
+    if (users != 1 || pool < 0) continue;
+    const int* q = pl->layers[pool].p;   // in, out, H, W, C, k, stride, pad, OH, OW
+    if (q[5] != 2 || q[6] != 2 || q[7] != 0 || q[8] * 2 != p[12] || q[9] * 2 != p[13]) continue;
+    Lc.pool2_op = pool;
     pl->layers[pool].fused = true;
     pl->virt[t] = 1;
   }
@@ -1078,6 +1118,7 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
     a.S = Sf;
     a.CG = C / 64;
     a.x0 = a.y0 = -pad;
+    a.pool2 = L.pool2_op >= 0 ? 1 : 0;   // band_config: even band heights, streamed weights
   }
   const int bn = N % 256 == 0 ? 256 : N % 128 == 0 ? 128 : 64;
   if (cgw == 16 && bn > 128) return 0;
@@ -1099,16 +1140,19 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
     a.PW = q[9];
     if (!stem_pool_config(a))
       return -fail(B2_ERR_UNSUPPORTED, "layer %zu: fused stem/max-pool geometry rejected", li);
-  } else if (!band_config(a, bn, cgw) || !band_supported(a, bn, cgw, a.act)) {
+  } else if ((L.pool2_op >= 0 && a.Wp > 128) || !band_config(a, bn, cgw) ||
+             !band_supported(a, bn, cgw, a.act)) {
     // rows too wide for one band pitch (VGG 224x224): split each row into two
-    // column segments of pitch 128 (126 valid columns + halo)
+    // column segments of pitch 128 (126 valid columns + halo).  The fused
+    // 2x2 pool needs exactly one output row per M tile, so it always splits.
     if (L.s2d || a.Wp <= 128 || OW > 2 * (128 - (Sf - 1))) return 0;
     a.Wp = 128;
     a.seg_w = 128 - (Sf - 1);
     a.nseg = (OW + a.seg_w - 1) / a.seg_w;
     if (!band_config(a, bn, cgw) || !band_supported(a, bn, cgw, a.act)) return 0;
   }
-  if (L.pool_op < 0 && (long)a.B * a.nbands * a.tiles_n < pl->num_sms) {   // small batch: more, smaller units
+  if (L.pool_op < 0 && L.pool2_op < 0 &&
+      (long)a.B * a.nbands * a.tiles_n < pl->num_sms) {   // small batch: more, smaller units
     BandArgs t = a;
     if (band_config(t, bn, cgw, 1) && band_supported(t, bn, cgw, t.act)) a = t;
   }
@@ -1117,11 +1161,23 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
   // ResNet layer1 3x3 b=256 69 -> 66 us; VGG 224x224 (two column segments per
   // row) 1.05 -> 1.34 ms, so single-segment rows only
   if (pl->band_pair && cgw == 64 && bn == 64 && a.CG == 1 && a.b_resident && a.tiles_n == 1 &&
-      a.R == 3 && a.S == 3 && L.pool_op < 0 && a.nseg == 1 &&
+      a.R == 3 && a.S == 3 && L.pool_op < 0 && L.pool2_op < 0 && a.nseg == 1 &&
       (long)a.B * a.nbands * a.nseg >= pl->num_sms) {
     BandArgs t = a;
     t.pair = 1;
     if (band_smem_bytes(t, 64) <= 232448) a = t;
+  }
+  if (L.pool2_op >= 0) {
+    // the pool is already marked fused: this layer must take the pooling band path
+    for (int cap = a.MT; (a.bh & 1) && cap > 1; --cap) {
+      BandArgs t = a;
+      if (band_config(t, bn, cgw, cap - 1) && band_supported(t, bn, cgw, t.act)) a = t;
+    }
+    if (a.Wp != 128 || (a.bh & 1) || a.R != 3 || a.act != ACT_RELU || a.b_resident || bn != 128)
+      return -fail(B2_ERR_UNSUPPORTED,
+                   "layer %zu: fused 2x2 max-pool band geometry rejected (Wp %d bh %d bn %d "
+                   "resident %d CG %d act %d)", li, a.Wp, a.bh, bn, a.b_resident, a.CG, a.act);
+    a.pool2 = 1;
   }
   EncodeTiledFn fn = encode_fn();
   if (!fn) return -fail(B2_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -1145,13 +1201,19 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
     return -fail(B2_ERR_CUDA, "layer %zu: band B tensor map rejected", li);
   // output NHWC [B, OH, OW, N]: 32-channel x 32-pixel boxes, 64 B swizzle;
   // one map per column segment, each clipping at its own width
+  // fused 2x2 pool: the maps describe the pooled tensor [B, OH/2, OW/2, N]
+  // (16-pixel boxes), segment column offsets halved
+  const int dv = a.pool2 ? 2 : 1;
+  void* obase = a.pool2 ? S.act[pl->layers[L.pool2_op].p[1]] : S.act[p[1]];
   for (int sg = 0; sg < a.nseg && sg < 2; ++sg) {
     const int w0 = sg * a.seg_w, wn = sg + 1 < a.nseg ? a.seg_w : OW - w0;
-    cuuint64_t odims[4] = {(cuuint64_t)N, (cuuint64_t)wn, (cuuint64_t)OH, (cuuint64_t)batch};
-    cuuint64_t ostr[3] = {(cuuint64_t)N * 2, (cuuint64_t)OW * N * 2, (cuuint64_t)OH * OW * N * 2};
-    cuuint32_t obox[4] = {32, 32, 1, 1};
+    cuuint64_t odims[4] = {(cuuint64_t)N, (cuuint64_t)(wn / dv), (cuuint64_t)(OH / dv),
+                           (cuuint64_t)batch};
+    cuuint64_t ostr[3] = {(cuuint64_t)N * 2, (cuuint64_t)(OW / dv) * N * 2,
+                          (cuuint64_t)(OH / dv) * (OW / dv) * N * 2};
+    cuuint32_t obox[4] = {32, (cuuint32_t)(32 / dv), 1, 1};
     CUtensorMap* m = sg == 0 ? &S.tmO[li] : &S.tmT[li];
-    if (fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, static_cast<bf16*>(S.act[p[1]]) + (size_t)w0 * N,
+    if (fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, static_cast<bf16*>(obase) + (size_t)(w0 / dv) * N,
            odims, ostr, obox, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return -fail(B2_ERR_CUDA, "layer %zu: band output tensor map rejected", li);
@@ -1238,6 +1300,8 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     if (brc == 1) continue;
     if (L.band8)   // its weights are in the paired-tap layout only conv_band reads
       return fail(B2_ERR_UNSUPPORTED, "layer %zu: 8-channel band conv geometry rejected", li);
+    if (L.pool2_op >= 0)   // its max-pool was fused away at plan creation
+      return fail(B2_ERR_UNSUPPORTED, "layer %zu: fused 2x2 max-pool needs the band kernel", li);
     brc = plan_chain_state(pl, S, li, batch);
     if (brc < 0) return -brc;
     if (brc == 1) continue;

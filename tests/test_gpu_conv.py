@@ -401,3 +401,48 @@ def test_band_pair(gpu_required, monkeypatch, H, W, batch, pair):
     bands, each CTA holding half of the resident weights) and the single-CTA one."""
     monkeypatch.setenv("B2_BAND_PAIR", pair)
     check(conv_plan(H, W, 64, 64, 3, 1), batch)
+
+
+def conv_pool2_plan(H, W, C, N, seed=0):
+    """3x3/1 conv (ReLU) then a 2x2/2 max-pool: VGG's block ends."""
+    b = P.PlanBuilder("conv_pool2")
+    x = b.tensor(H, W, C)
+    b.in_elems = C * H * W
+    b.op_p(P.OP_INPUT, [x, C, H, W, C])
+    rng = np.random.default_rng(seed)
+    y = b.tensor(H, W, N)
+    w = rng.standard_normal((N, 3, 3, C)) * (1.0 / np.sqrt(9 * C))
+    b.op_p(P.OP_CONV, [x, y, b.weight(w), b.weight(rng.standard_normal(N) * 0.1), H, W, C, N,
+                       3, 3, 1, 1, H, W, 1, -1])
+    z = b.tensor(H // 2, W // 2, N)
+    b.op_p(P.OP_MAXPOOL, [y, z, H, W, N, 2, 2, 0, H // 2, W // 2])
+    b.out_elems = b.tensors[z].elems
+    b.op_p(P.OP_OUTPUT, [1, z, 0])
+    return b.build(P.DT_FP32)
+
+
+@pytest.mark.parametrize("H,W,C,N,batch", [
+    (224, 224, 64, 128, 2),    # two column segments per row
+    (112, 112, 64, 128, 3),
+    (112, 112, 128, 128, 2),   # VGG conv2_2 + pool2
+    (100, 120, 64, 128, 3),    # ragged band tail, W below one pitch
+    (224, 224, 64, 64, 2),     # N = 64: not fused (the pool runs as its own kernel)
+])
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_band_maxpool2(gpu_required, monkeypatch, H, W, C, N, batch, fused):
+    """Band conv with the 2x2/2 max-pool fused into its epilogue (the conv
+    output is never materialised) and unfused."""
+    monkeypatch.setenv("B2_POOL_FUSION", fused)
+    blob = conv_pool2_plan(H, W, C, N)
+    pl = P.decode(blob)
+    x = plan_ref.make_inputs(pl, batch, 5)
+    plan = R.Plan(blob, P.DT_BF16)
+    try:
+        out = plan.predict(x)
+        assert np.isfinite(out).all()
+        rt = lambda t: plan.read_tensor(batch, t, pl.tensors[t].elems, pl.tensors[t].kind)
+        assert (rt(pl.ops[1][1]) is None) == (fused == "1" and N == 128)
+        errs = plan_ref.layerwise_errors(pl, rt, x, True)
+        assert errs and all(e[2] <= TOL for e in errs), errs
+    finally:
+        plan.close()
