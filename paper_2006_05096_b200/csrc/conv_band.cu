@@ -71,6 +71,28 @@ B2_DEV uint64_t band_adesc(uint32_t addr) {
 // keep up with 64-cycle (N <= 128) / 128-cycle (N = 256) MMAs, and a loop with
 // runtime tap decomposition (integer division, parameter reloads) measured
 // ~170 cycles per MMA — the tensor pipe then idles 80% of the time.
+// CTA-local unit sequence: normally unit blockIdx.x + k * gridDim.x.  With
+// the fused 2x2 pool on one-row bands (POOL, bh == 1) a CTA takes row PAIRS:
+// its k-th unit is row (k & 1) of band pair blockIdx.x + (k >> 1) * gridDim.x,
+// so the epilogue meets both rows of every pooled row (nbands is even).
+template <bool POOL>
+B2_DEV int band_unit(const BandArgs& a, int k, int units) {
+  if (!POOL || a.bh != 1) {
+    const long u = blockIdx.x + (long)k * gridDim.x;
+    return u < units ? (int)u : -1;
+  }
+  const long pp = blockIdx.x + (long)(k >> 1) * gridDim.x;
+  if (pp >= units / 2) return -1;
+  const int nt = (int)(pp % a.tiles_n);
+  long rest = pp / a.tiles_n;
+  const int seg = (int)(rest % a.nseg);
+  rest /= a.nseg;
+  const int bp = (int)(rest % (a.nbands / 2));
+  const int img = (int)(rest / (a.nbands / 2));
+  const int band = 2 * bp + (k & 1);
+  return ((img * a.nbands + band) * a.nseg + seg) * a.tiles_n + nt;
+}
+
 template <int BN, int CGW, int R, int S, bool BRES, int ACT, bool POOL = false>
 __global__ void __launch_bounds__(CB_THREADS, 1)
     conv_band_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -140,7 +162,9 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
       }
       int as = 0, bs = 0;
       uint32_t aph = 0, bph = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int k = 0;; ++k) {
+        const int u = band_unit<POOL>(a, k, units);
+        if (u < 0) break;
         const int nt = u % a.tiles_n;
         const int rest = u / a.tiles_n;
         const int seg = rest % a.nseg;
@@ -188,7 +212,9 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
     int as = 0, bs = 0;
     uint32_t aph = 0, bph = 0;
     int it = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+    for (int k = 0;; ++k, ++it) {
+      const int u = band_unit<POOL>(a, k, units);
+      if (u < 0) break;
       const int seg = (u / a.tiles_n) % a.nseg;
       const int band = (u / a.tiles_n / a.nseg) % a.nbands;
       const int vr = min(a.bh, a.H - band * a.bh);
@@ -285,7 +311,10 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
     float bpre[32];
     int bpre_n0 = -1;
     int it = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+    float prow[32];   // POOL, one-row bands: the pair's top row, post-activation
+    for (int k = 0;; ++k, ++it) {
+      const int u = band_unit<POOL>(a, k, units);
+      if (u < 0) break;
       const int nt = u % a.tiles_n;
       const int rest = u / a.tiles_n;
       const int seg = rest % a.nseg;
@@ -318,6 +347,51 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
         // rows 2j, 2j+1 meet in registers, column pairs across lanes 2i, 2i+1;
         // even lanes stage 16 pooled pixels x 32 channels, one TMA store
         const int segw0 = seg < a.nseg - 1 ? a.seg_w : a.W - seg * a.seg_w;
+        if (a.bh == 1) {
+          // rows meet across consecutive units (band_unit pairs them); BN = 64:
+          // one 32-column chunk per warp
+          const int p0 = q * 32;
+          const int c = eh * 32;
+          uint32_t ra[32];
+          tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + ab * a.MT * BN + c, ra);
+          tmem_wait_ld();
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = act_t<ACT>(__uint_as_float(ra[j]) + bpre[j]);
+          if ((k & 1) == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) prow[j] = v[j];
+          } else if (n0 + c < a.N) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float m = fmaxf(v[j], prow[j]);
+              v[j] = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+            }
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            uint8_t* sbuf = obuf + (oi & 1) * 2048;
+            if ((lane & 1) == 0) {
+              const int pr = lane >> 1;
+              const uint32_t pswz = (pr >> 1) & 3;
+              uint8_t* orow = sbuf + pr * 64;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                uint4 w;
+                w.x = pack_bf16x2(v[8 * j + 0], v[8 * j + 1]);
+                w.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
+                w.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
+                w.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
+                *reinterpret_cast<uint4*>(orow + ((j ^ pswz) << 4)) = w;
+              }
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && p0 < segw0)
+              tma_store_4d(omap, sbuf, n0 + c, p0 >> 1, band >> 1, img);
+            if (lane == 0) bulk_commit();
+            ++oi;
+          }
+        } else
         for (int mt = 0; mt + 1 < mt_valid; mt += 2) {
           const int r = mt;                              // band row of the pair's top
           if (r + 1 >= vr) break;
@@ -734,7 +808,7 @@ bool band_config(BandArgs& a, int bn, int cgw, int mt_cap) {
     int bh = (mt * 128) / a.Wp;
     if (bh < 1) continue;
     if (bh > a.H) bh = a.H;
-    if (a.pool2 && (bh & 1)) continue;   // fused 2x2 pool: whole row pairs per band
+    if (a.pool2 && bh > 1 && (bh & 1)) continue;   // fused 2x2 pool: row pairs in or across bands
     const int bands = (a.H + bh - 1) / bh;
     double computed = 0.0;
     for (int b = 0; b < bands; ++b) {
@@ -748,9 +822,7 @@ bool band_config(BandArgs& a, int bn, int cgw, int mt_cap) {
     t.b_resident = 1;
     t.b_stages = 0;
     t.a_stages = 2;
-    // instantiated resident kernels (the pooling epilogue streams its weights:
-    // resident 3x3x64x64 leaves room only for one-row bands)
-    const bool res_ok = a.tiles_n == 1 && a.CG == 1 && bn == 64 && !a.pool2;
+    const bool res_ok = a.tiles_n == 1 && a.CG == 1 && bn == 64;   // instantiated resident kernels
     (void)0;
     if (res_ok && band_smem_bytes(t, bn) <= CB_SMEM_MAX) {
       c.res = 1;
@@ -841,6 +913,8 @@ static cudaError_t band_dispatch(const BandArgs& a, int bn, int cgw, const CUten
   }
   if (a.pool2) {   // fused 2x2 max-pool (VGG): ReLU only (checked on the host)
     if constexpr (ACT == ACT_RELU) {
+      if (bn == 64 && a.b_resident && a.CG == 1 && a.bh == 1)
+        return band_launch_t<64, 64, 3, 3, true, ACT_RELU, true>(a, ta, tb, to, to2, num_sms, st);
       if (bn == 128 && !a.b_resident)
         return band_launch_t<128, 64, 3, 3, false, ACT_RELU, true>(a, ta, tb, to, to2, num_sms, st);
     }

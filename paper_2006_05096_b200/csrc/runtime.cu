@@ -436,16 +436,16 @@ void plan_fuse_pool(b2_plan* pl) {
   // 3x3/1 band convs (VGG) followed by a 2x2/2 max-pool that is their only
   // consumer: the band epilogue pools row pairs / column pairs and writes only
   // the pooled tensor (needs one output row per M tile: band pitch 128).
-  // N = 128 only (streamed weights either way; measured VGG conv2_2 + pool2
-  // 0.811 + 0.237 -> 0.795 ms).  At N = 64 the even band height forces the
-  // weights out of shared memory: conv1_2 1.06 -> 1.64 ms, more than pool1's
-  // 0.46 ms saved.
+  // N = 128 (streamed weights; VGG conv2_2 + pool2 0.811 + 0.237 -> 0.795 ms)
+  // pairs rows inside a band; N = 64 keeps its resident weights with one-row
+  // bands and pairs rows across consecutive units of a CTA (an even band
+  // height pushed the weights out of shared memory: conv1_2 1.06 -> 1.64 ms).
   for (size_t ci = 0; ci < pl->layers.size() && pl->dtype == B2_DT_BF16; ++ci) {
     Layer& Lc = pl->layers[ci];
     const int* p = Lc.p;
     if (Lc.kind != OP_CONV || Lc.s2d || Lc.pool_op >= 0 || p[14] != ACT_RELU || p[15] >= 0 ||
         p[8] != 3 || p[9] != 3 || p[10] != 1 || p[11] != 1 || p[6] % 64 != 0 ||
-        p[7] != 128 || p[7] > pl->band_max_n || p[12] != p[4] ||
+        !(p[7] == 64 || p[7] == 128) || p[7] > pl->band_max_n || p[12] != p[4] ||
         p[13] != p[5] || (p[12] & 1) || (p[13] & 1) || p[13] + 2 <= 96 || p[13] > 2 * 126)
       continue;
     const int t = p[1];
@@ -1169,11 +1169,9 @@ int plan_band(b2_plan* pl, BatchState& S, size_t li, int batch) {
   }
   if (L.pool2_op >= 0) {
     // the pool is already marked fused: this layer must take the pooling band path
-    for (int cap = a.MT; (a.bh & 1) && cap > 1; --cap) {
-      BandArgs t = a;
-      if (band_config(t, bn, cgw, cap - 1) && band_supported(t, bn, cgw, t.act)) a = t;
-    }
-    if (a.Wp != 128 || (a.bh & 1) || a.R != 3 || a.act != ACT_RELU || a.b_resident || bn != 128)
+    if (a.Wp != 128 || (a.bh > 1 && (a.bh & 1)) || (a.bh == 1 && (a.nbands & 1)) || a.R != 3 ||
+        a.act != ACT_RELU ||
+        !((bn == 64 && a.b_resident && a.CG == 1 && a.bh == 1) || (bn == 128 && !a.b_resident)))
       return -fail(B2_ERR_UNSUPPORTED,
                    "layer %zu: fused 2x2 max-pool band geometry rejected (Wp %d bh %d bn %d "
                    "resident %d CG %d act %d)", li, a.Wp, a.bh, bn, a.b_resident, a.CG, a.act);
