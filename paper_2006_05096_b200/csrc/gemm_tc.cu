@@ -654,8 +654,8 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
     stamp(5);
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    printf("b2ts %d %u %llu %llu %llu %llu %llu %llu\n", blockIdx.x, smid, ts[0], ts[1], ts[2],
-           ts[3], ts[4], ts[5]);
+    printf("b2ts %d %u %llu %llu %llu %llu %llu %llu stages %d kblocks %d tiles %d\n", blockIdx.x,
+           smid, ts[0], ts[1], ts[2], ts[3], ts[4], ts[5], STAGES, a.kblocks, ntiles);
 #ifdef B2_TILE_TS
     if (a.ts_debug == 2 && blockIdx.x == 0)
 #else
