@@ -780,8 +780,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<BN>::THREADS,
           uint8_t* dB = sB + stage * Cfg::B_BYTES;
           if (kb >= a.kblocks) {
             const int j = kb - a.kblocks;
-            tma_load_2d_pair(dA, &tmR, fl, n0 + j * TC_BK, m0);
-            tma_load_2d_pair(dB, &tmI, fl, j * TC_BK, (int)rank * (BN / 2));
+            if (a.fold_kind == 0) {   // residual x identity (this CTA's half of the rows)
+              tma_load_2d_pair(dA, &tmR, fl, n0 + j * TC_BK, m0);
+              tma_load_2d_pair(dB, &tmI, fl, j * TC_BK, (int)rank * (BN / 2));
+            } else {                  // folded projection shortcut: x (or strided x) x Wd
+              if (a.fold_kind == 1) {
+                tma_load_2d_pair(dA, &tmR, fl, j * TC_BK, m0);
+              } else {
+                const int im = m0 / a.OHW;
+                const int rem = m0 - im * a.OHW;
+                const int oh = rem / a.OW;
+                tma_load_im2col_4d_pair(dA, &tmR, fl, j * TC_BK, (rem - oh * a.OW) * a.stride,
+                                        oh * a.stride, im, 0, 0);
+              }
+              tma_load_2d_pair(dB, &tmI, fl, j * TC_BK, nb);
+            }
           } else {
             if (a.a_im2col) {
               const int tap = kb / cpb;

@@ -1315,12 +1315,13 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     // CTA-pair (cta_group::2) GEMM vs single CTA and the tile width: per-SM
     // clock model in tc_pick_config (TMA fill rate vs MMA vs epilogue writes).
     // Pairs need a TMA-fed A (no gather / s2d / folded shortcut).
-    const bool pair_allowed = pl->use_pair && !L.s2d && !L.gather && L.ds_op < 0 &&
+    const bool pair_allowed = pl->use_pair && !L.s2d && !L.gather &&
                               (!L.im2col || L.im2col_mode == 1) && N % 8 == 0 &&
                               M >= pl->pair_min_m && L.K >= pl->pair_min_k;
     const int res_in = conv ? p[15] : p[8];
+    const int ds_kb = L.ds_op >= 0 ? pl->layers[L.ds_op].kpad / 64 : 0;   // folded shortcut K
     bool pair_ok = false;
-    int bn = tc_pick_config(M, N, L.kpad / 64, res_in >= 0 && L.K <= pl->fold_max_k,
+    int bn = tc_pick_config(M, N, L.kpad / 64 + ds_kb, res_in >= 0 && L.K <= pl->fold_max_k,
                             pl->num_sms, pair_allowed, &pair_ok);
     // Memory-bound shapes (one K block, or im2col A that each extra N tile
     // re-gathers) want the widest tile: measured 56x56x64->256 128 -> 115 us,

@@ -212,6 +212,9 @@ def shortcut_plan(H, C, Cm, N, stride, seed=0):
     (56, 64, 64, 256, 1, 6),      # ResNet layer1 block 0
     (56, 256, 128, 512, 2, 4),    # layer2 block 0 (strided shortcut via im2col TMA)
     (14, 1024, 512, 2048, 2, 8),  # layer4 block 0
+    (56, 256, 128, 512, 2, 8),    # M >= 4096: the CTA-pair GEMM with the folded shortcut
+    (28, 512, 256, 1024, 2, 24),  # layer3 block 0, pair
+    (14, 1024, 512, 2048, 2, 96), # layer4 block 0, pair
 ])
 @pytest.mark.parametrize("fold", ["1", "0"])
 def test_shortcut_fold(gpu_required, monkeypatch, H, C, Cm, N, stride, batch, fold):
