@@ -67,7 +67,7 @@ B2_DEV void add_bf16x8(float* v, const uint4& u) {
 // B2_GEMM_TS=2: per-tile stamps of CTA 0's first 32 tiles (globaltimer, ns):
 // [0] producer past empty-wait, [1] MMA past full-wait, [2] MMA commits issued,
 // [3] epilogue warp 2 past tfull-wait, [4] epilogue warp 2 arrived tempty
-__device__ unsigned long long g_tile_ts[5][32];
+__device__ unsigned long long g_tile_ts[6][32];
 // Compiled in only with -DB2_TILE_TS: the lane-0 branches inside the MMA issue
 // loop cost ~7% on single-K-block GEMMs (they break the converged issuer).
 B2_DEV void tile_stamp(const TcArgs& a, int which, int tile) {
@@ -315,6 +315,9 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
           iw0 = (rem - oh * a.OW) * a.stride - a.pad;
         }
         for (int kb = kb0; kb < kb1; ++kb) {
+#ifdef B2_TILE_TS
+          if (kb == kb0 && a.ts_debug == 2) tile_stamp(a, 5, (u - (int)blockIdx.x) / (int)gridDim.x);
+#endif
           mbar_wait(&empty[stage], phase ^ 1);
 #ifdef B2_TILE_TS
           if (kb == kb0 && a.ts_debug == 2) tile_stamp(a, 0, (u - (int)blockIdx.x) / (int)gridDim.x);
@@ -662,8 +665,8 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
     if (false)
 #endif
       for (int t = 0; t < 32; ++t)
-        printf("b2tile %d %llu %llu %llu %llu %llu\n", t, g_tile_ts[0][t], g_tile_ts[1][t],
-               g_tile_ts[2][t], g_tile_ts[3][t], g_tile_ts[4][t]);
+        printf("b2tile %d %llu %llu %llu %llu %llu %llu\n", t, g_tile_ts[0][t], g_tile_ts[1][t],
+               g_tile_ts[2][t], g_tile_ts[3][t], g_tile_ts[4][t], g_tile_ts[5][t]);
   }
   if (warp == 1) {
     tc_fence_after();
