@@ -73,11 +73,12 @@ int main() {
   void* wbuf;
   cudaMalloc(&wbuf, 1 << 20);
   cudaMemset(wbuf, 1, 1 << 20);
-  for (int wbox : {0, 32, 64})
+  for (int oob : {0, 1})
+  for (int wbox : {0, 32})
   for (int box_rows : {128}) {
     CUtensorMap tm, tw;
     {
-      cuuint64_t wd[2] = {64, 4096};
+      cuuint64_t wd[2] = {64, (cuuint64_t)(oob ? 16 : 4096)};
       cuuint64_t wst[1] = {128};
       cuuint32_t wb[2] = {64, (cuuint32_t)(wbox ? wbox : 32)};
       cuuint32_t wes[2] = {1, 1};
@@ -85,14 +86,17 @@ int main() {
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
-    cuuint64_t dims[2] = {64, rows};
-    cuuint64_t str[1] = {128};
+    // oob = 1: a 32-column (64 B) tensor read with the 64-column box, half of
+    // every box row out of bounds (the narrow-K GEMM A operand); weights box
+    // of 32 rows over a 16-row tensor
+    cuuint64_t dims[2] = {(cuuint64_t)(oob ? 32 : 64), oob ? rows * 2 : rows};
+    cuuint64_t str[1] = {(cuuint64_t)(oob ? 64 : 128)};
     cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
     enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, str, box, es,
         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    const int tiles = (int)(rows / box_rows);
+    const int tiles = (int)((oob ? rows * 2 : rows) / box_rows);
     for (int stages : {2, 4, 8}) {
       const int smem = stages * (box_rows + wbox) * 128 + 2048;
       if (smem > 232448) continue;
@@ -103,7 +107,7 @@ int main() {
       cudaEventSynchronize(e1);
       float ms = 0;
       cudaEventElapsedTime(&ms, e0, e1);
-      printf("wbox %2d  box %3d rows (%3d KB) stages %2d (%4d KB in flight/SM): %7.1f GB/s  (%s)\n", wbox, box_rows,
+      printf("oob %d wbox %2d  box %3d rows (%3d KB) stages %2d (%4d KB in flight/SM): %7.1f GB/s  (%s)\n", oob, wbox, box_rows,
              box_rows * 128 / 1024, stages, stages * box_rows * 128 / 1024,
              5.0 * bytes / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
     }
