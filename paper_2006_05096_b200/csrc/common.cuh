@@ -169,6 +169,27 @@ B2_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------- async copies
+// K-major operand descriptors for narrow rows: 64-byte (32 bf16) rows with
+// 64B swizzle (SBO = 8 rows x 64 B) and 32-byte (16 bf16) rows with 32B swizzle
+B2_DEV uint64_t smem_desc_sw64_k(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;   // SWIZZLE_64B
+  return d;
+}
+B2_DEV uint64_t smem_desc_sw32_k(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;   // SWIZZLE_32B
+  return d;
+}
+
 B2_DEV void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

@@ -375,7 +375,9 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
               tma_load_im2col_4d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], c0, iw0, ih0,
                                  img, (uint16_t)s, (uint16_t)r);
             } else {
-              mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
+              // narrow K: the A box is a_narrow elements wide (no out-of-bounds fill)
+              mbar_arrive_expect_tx(&full[stage], (a.a_narrow ? TC_BM * a.a_narrow * 2
+                                                               : Cfg::A_BYTES) + Cfg::B_BYTES);
               tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * TC_BK, m0);
             }
             tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * TC_BK, n0);
@@ -411,14 +413,18 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
           if (kb == kb0 && lane == 0) tile_stamp(a, 1, it);
 #endif
           const bool tap8 = a.a_im2col == 2 && kb < a.kblocks;
+          const bool narrow = a.a_narrow && kb < a.kblocks;
           const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
           const uint64_t ad = tap8 ? smem_desc_kmajor_noswizzle(a_addr, 2048, 128)
-                                   : smem_desc_sw128(a_addr);
+                              : narrow ? (a.a_narrow == 32 ? smem_desc_sw64_k(a_addr)
+                                                           : smem_desc_sw32_k(a_addr))
+                                       : smem_desc_sw128(a_addr);
           const uint32_t astep = tap8 ? 256u : 2u;   // K += 16: 2 taps (4 KB) or 32 B
+          const int ksteps = narrow ? a.a_narrow / 16 : TC_BK / 16;
           const uint64_t bd = smem_desc_sw128(smem_u32(sB + stage * Cfg::B_BYTES));
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k)
-            if (elect_one())
+            if (k < ksteps && elect_one())
               umma_bf16(dt, ad + astep * k, bd + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           if (elect_one()) umma_commit(&empty[stage]);
           if (++stage == STAGES) {

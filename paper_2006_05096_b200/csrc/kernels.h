@@ -32,6 +32,7 @@ struct TcArgs {
   int tma_epi;          // epilogue through smem + TMA store (N % 8 == 0, BN >= 64)
   int stages;           // smem pipeline depth (0 = the most that fits)
   int epi_debug;        // 0 normal; 1 drain TMEM only (no math/stores) — profiling aid
+  int a_narrow;         // K <= 32 plain GEMM: A boxes 32 (SW64) or 16 (SW32) elements wide, not 64
   int ts_debug;         // B2_GEMM_TS=1: first/last CTA print phase timestamps — profiling aid
   int OH;               // s2d stems: output rows per image (M tile = one output row)
   int out3d;            // output TMA map is [rows, OW, C]: box rows clip at OW

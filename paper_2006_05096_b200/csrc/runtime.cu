@@ -246,6 +246,7 @@ struct BatchState {
   std::vector<CUtensorMap> tmO;    // per layer (tc): output, 32x32 box, 64B swizzle
   std::vector<CUtensorMap> tmR;    // per layer (tc, residual fold): residual as an A operand
   std::vector<char> fold;          // per layer: residual folded into the MMA
+  std::vector<char> a_narrow;      // per layer: A box width for K <= 32 (0 = 64)
   std::vector<CUtensorMap> tmI;    // per layer: identity [256 x 256] (box rows = BN) for the fold
   std::vector<char> band;          // per layer: banded implicit-GEMM conv (conv_band.cu)
   std::vector<char> pair;          // per layer: CTA-pair GEMM (tc_gemm2_kernel)
@@ -296,6 +297,7 @@ struct b2_plan {
   bool use_band = true;      // B2_BAND=0 -> stride-1 k x k convs and s2d stems on gemm_tc
   bool use_pair = true;      // B2_PAIR=0 -> single-CTA tc_gemm only
   bool band_pair = true;     // B2_BAND_PAIR=0 -> single-CTA band kernel for N = 64
+  bool narrow_k = true;      // B2_NARROW_K=0 -> 64-wide A boxes for K <= 32 too
   bool verbose = false;      // B2_VERBOSE=1: per-layer kernel choices on stderr
   long pair_min_m = 4096;    // B2_PAIR_MIN_M: smallest M sent to the CTA-pair GEMM
   int pair_min_k = 0;        // B2_PAIR_MIN_K: shortest K sent to the CTA-pair GEMM
@@ -886,6 +888,7 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
             a.SC = p[9] * p[6];
           }
           a.tma_epi = bn >= 32 && N % 8 == 0 && pl->epi_mode != 2;
+          a.a_narrow = S.a_narrow[li];
           a.epi_debug = pl->epi_mode == 2 ? 0 : pl->epi_mode;
           a.ts_debug = pl->ts_debug;
           a.stages = pl->stages_override;
@@ -1257,6 +1260,7 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
   S.tmO.resize(pl->layers.size());
   S.tmR.resize(pl->layers.size());
   S.fold.assign(pl->layers.size(), 0);
+  S.a_narrow.assign(pl->layers.size(), 0);
   S.tmI.resize(pl->layers.size());
   S.band.assign(pl->layers.size(), 0);
   S.pair.assign(pl->layers.size(), 0);
@@ -1408,7 +1412,17 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
       const int K = L.K;
       const long ld = conv ? p[6] : p[9];
       if ((ld * 2) % 16 != 0) return fail(B2_ERR_UNSUPPORTED, "layer %zu: A pitch not 16B", li);
-      if (!make_tmap_bf16(&S.tmA[li], S.act[p[0]], (uint64_t)M, (uint64_t)K, (uint64_t)ld * 2, 128))
+      // K <= 32 on the single-CTA kernel: a 32- or 16-wide A box (64 B / 32 B
+      // swizzle) instead of a half-empty 64-wide one — measured, boxes with
+      // out-of-bounds halves stream at ~60% of the in-bounds rate
+      const int nar = (pl->narrow_k && !S.pair[li] && S.split[li] == 1 && K <= 32)
+                          ? (K <= 16 ? 16 : 32) : 0;
+      S.a_narrow[li] = (char)nar;
+      if (!make_tmap_bf16(&S.tmA[li], S.act[p[0]], (uint64_t)M, (uint64_t)K, (uint64_t)ld * 2, 128,
+                          nar ? nar : 64,
+                          nar == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                    : nar == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                : CU_TENSOR_MAP_SWIZZLE_128B))
         return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeTiled(A) failed", li);
     }
   }
@@ -1520,6 +1534,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* bd = getenv("B2_BAND")) pl->use_band = bd[0] != '0';
   if (const char* pr = getenv("B2_PAIR")) pl->use_pair = pr[0] != '0';
   if (const char* bp = getenv("B2_BAND_PAIR")) pl->band_pair = bp[0] != '0';
+  if (const char* nk = getenv("B2_NARROW_K")) pl->narrow_k = nk[0] != '0';
   if (const char* vb = getenv("B2_VERBOSE")) pl->verbose = vb[0] == '1';
   if (const char* pm = getenv("B2_PAIR_MIN_M")) pl->pair_min_m = atol(pm);
   if (const char* pk = getenv("B2_PAIR_MIN_K")) pl->pair_min_k = atoi(pk);

@@ -163,6 +163,9 @@ def linear_plan(K, N, res, seed=0):
     (8192, 1024, 256, False),
     (6000, 512, 192, False),    # N not a multiple of the tile: BN = 128, ragged N
     (50176, 64, 256, True),
+    (5000, 16, 96, False),      # K <= 32: narrow A boxes (16-wide, 32B swizzle)
+    (3000, 24, 144, True),      #   24 -> 32-wide box, 8 zero-filled columns, residual fold
+    (7000, 32, 16, False),      #   32-wide (64B swizzle), BN = 32 for N = 16
 ])
 @pytest.mark.parametrize("pair", ["1", "0"])
 def test_gemm_shapes(gpu_required, monkeypatch, M, K, N, res, pair):

@@ -1,5 +1,4 @@
-# narrow-N memory-bound GEMM (MobileNet 112x112x32 -> 16): which epilogue step paces the tiles
+# narrow-K GEMMs (MobileNet 1x1 shapes): 64-wide vs narrow A boxes
 cd $GRAFT_REPO_ROOT
 M=3211264
-for e in 0 1 3 4 5 6; do B2_EPI_MODE=$e python tools/gemm_micro.py $M 32 16; done
-for e in 0 1 4 5; do B2_EPI_MODE=$e python tools/gemm_micro.py 802816 64 64; done
+for s in "32 16" "16 96" "24 144" "32 192"; do python tools/gemm_micro.py $M $s; B2_NARROW_K=0 python tools/gemm_micro.py $M $s; done
