@@ -19,6 +19,8 @@
  *                    (hot loop :217-231) -> per-request latency + completion ms,
  *                    the LatencySamples fields of profiler/stats.py:21-38
  *   b2_gen_input     build_payload (synthetic request bodies) profiler/clients.py:153-158
+ *   b2_plan_memory   ProcessStatsReader.read's memory figure for the instance
+ *                    (RSS there, device bytes here)          telemetry/providers.py:147-170
  *   b2_plan_destroy  MockServer.shutdown                    mockserve/server.py:132-134
  *   b2_last_error    the exception text the reference raises (ToyFormatError,
  *                    RequestFailure, ...) errors.py
@@ -114,6 +116,11 @@ B2_API int b2_profile_ops(b2_plan* plan, int batch, int iters, float* op_ms, int
  * (the stem output under the fused stem/max-pool, a ResNet projection
  * shortcut folded into its block's last conv). */
 B2_API int b2_read_tensor(b2_plan* plan, int batch, int tensor, void* host_out, size_t bytes);
+
+/* Device memory the plan holds right now (weights, per-batch activation
+ * arenas, I/O buffers, split-K workspaces): the instance's memory indicator
+ * of a profiled cell (ProfilingResult.memory_bytes). */
+B2_API int b2_plan_memory(const b2_plan* plan, uint64_t* device_bytes);
 
 B2_API void b2_plan_destroy(b2_plan* plan);
 

@@ -311,6 +311,7 @@ struct b2_plan {
   void* identity = nullptr;  // bf16 I[256][256]
   void* stage = nullptr;     // weight-upload staging (plan creation only)
   size_t stage_bytes = 0;
+  size_t dev_bytes = 0;      // device memory held (weights, arenas, I/O buffers; b2_plan_memory)
   float* zero_bias = nullptr;  // fp32 zeros[8192]: bias of bias-free layers in fused epilogues
   int stages_override = 0;   // B2_STAGES
   int ts_debug = 0;          // B2_GEMM_TS
@@ -321,10 +322,17 @@ namespace {
 
 template <typename T> size_t tsize() { return sizeof(T); }
 
+// every plan-lifetime device allocation goes through here (b2_plan_memory)
+cudaError_t dmalloc(b2_plan* pl, void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaSuccess) pl->dev_bytes += bytes;
+  return e;
+}
+
 int upload_f32(b2_plan* pl, const float* src, size_t n, float** out) {
   float* d = nullptr;
   const size_t padded = (n + 255) / 256 * 256;   // epilogues read whole 32-column chunks
-  CK(cudaMalloc(&d, padded * sizeof(float)));
+  CK(dmalloc(pl, (void**)&d, padded * sizeof(float)));
   CK(cudaMemset(d, 0, padded * sizeof(float)));
   pl->allocs.push_back(d);
   CK(cudaMemcpy(d, src, n * sizeof(float), cudaMemcpyHostToDevice));
@@ -350,7 +358,7 @@ template <typename T> int upload_as(b2_plan* pl, const std::vector<float>& h, vo
   }
   CK(cudaMemcpy(pl->stage, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
   T* d = nullptr;
-  CK(cudaMalloc(&d, h.size() * sizeof(T) + 16));
+  CK(dmalloc(pl, (void**)&d, h.size() * sizeof(T) + 16));
   pl->allocs.push_back(d);
   CK(convert_f32<T>(static_cast<const float*>(pl->stage), d, (long)h.size(), 0));
   pl->weight_bytes += h.size() * sizeof(T);
@@ -1248,12 +1256,12 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     off[t] = arena;
     arena += (bytes + 256 + 1023) / 1024 * 1024;
   }
-  CK(cudaMalloc(&S.arena, arena));
+  CK(dmalloc(pl, (void**)&S.arena, arena));
   CK(cudaMemset(S.arena, 0, arena));
   for (size_t t = 0; t < pl->tensors.size(); ++t) S.act[t] = static_cast<uint8_t*>(S.arena) + off[t];
-  CK(cudaMalloc(&S.d_in, in_bytes(pl, batch) + 256));
+  CK(dmalloc(pl, (void**)&S.d_in, in_bytes(pl, batch) + 256));
   CK(cudaMemset(S.d_in, 0, in_bytes(pl, batch) + 256));
-  CK(cudaMalloc(&S.d_out, (size_t)batch * pl->out_elems * 4 + 256));
+  CK(dmalloc(pl, (void**)&S.d_out, (size_t)batch * pl->out_elems * 4 + 256));
   S.bn.assign(pl->layers.size(), 0);
   S.tmA.resize(pl->layers.size());
   S.tmB.resize(pl->layers.size());
@@ -1427,7 +1435,7 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     }
   }
   if (ws_elems) {
-    CK(cudaMalloc(&S.ws, ws_elems * sizeof(float) + 256));
+    CK(dmalloc(pl, (void**)&S.ws, ws_elems * sizeof(float) + 256));
     CK(cudaMemset(S.ws, 0, ws_elems * sizeof(float) + 256));
   }
   auto res = pl->states.emplace(batch, std::move(S));
@@ -1448,9 +1456,9 @@ int graph_of(b2_plan* pl, BatchState& S, cudaGraphExec_t* out, bool second = fal
     return B2_OK;
   }
   if (second && !S.d_in2) {
-    CK(cudaMalloc(&S.d_in2, in_bytes(pl, S.batch) + 256));
+    CK(dmalloc(pl, (void**)&S.d_in2, in_bytes(pl, S.batch) + 256));
     CK(cudaMemset(S.d_in2, 0, in_bytes(pl, S.batch) + 256));
-    CK(cudaMalloc(&S.d_out2, (size_t)S.batch * pl->out_elems * 4 + 256));
+    CK(dmalloc(pl, (void**)&S.d_out2, (size_t)S.batch * pl->out_elems * 4 + 256));
   }
   int rc;
   cudaGraph_t g;
@@ -1606,10 +1614,15 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
     pl->stage_bytes = 0;
   }
   if (!rc) {
-    // algorithmic FLOPs (2 per MAC) of the contraction ops
+    // algorithmic FLOPs (2 per MAC) of the contraction ops, with the model's
+    // true input channels (an image stem reads 3 channels padded to 8)
+    std::map<int, int> true_c;
+    for (const Layer& L : pl->layers)
+      if (L.kind == OP_INPUT) true_c[L.p[0]] = L.p[1];
     for (const Layer& L : pl->layers) {
       const int* p = L.p;
-      if (L.kind == OP_CONV) pl->flops += 2.0 * p[12] * p[13] * p[7] * p[8] * p[9] * p[6];
+      const int cin = true_c.count(p[0]) ? std::min(p[6], true_c[p[0]]) : p[6];
+      if (L.kind == OP_CONV) pl->flops += 2.0 * p[12] * p[13] * p[7] * p[8] * p[9] * cin;
       if (L.kind == OP_LINEAR) pl->flops += 2.0 * p[6] * p[5] * p[4];
       if (L.kind == OP_DWCONV) pl->flops += 2.0 * p[9] * p[10] * p[6] * p[12] * p[12];
       if (L.kind == OP_ATTENTION) pl->flops += 4.0 * p[2] * p[4] * p[4] * p[3];
@@ -1643,6 +1656,12 @@ int b2_plan_info(const b2_plan* pl, double* flops, double* wbytes, int* launches
     *launches = n;
   }
   if (dtype) *dtype = pl->dtype;
+  return B2_OK;
+}
+
+int b2_plan_memory(const b2_plan* pl, uint64_t* device_bytes) {
+  if (!pl || !device_bytes) return fail(B2_ERR_ARG, "null argument");
+  *device_bytes = pl->dev_bytes;
   return B2_OK;
 }
 

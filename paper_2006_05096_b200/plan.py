@@ -292,10 +292,11 @@ def with_dtype(blob: bytes, dtype: int) -> bytes:
 def flops_per_sample(plan: Plan) -> int:
     """Algorithmic multiply-add FLOPs (2 per MAC) of the contraction ops."""
     total = 0
+    true_c = {o[P_IN_OUT]: o[P_IN_C] for o in plan.ops if o.kind == OP_INPUT}
     for o in plan.ops:
         if o.kind == OP_CONV:
-            total += 2 * o[P_CV_OH] * o[P_CV_OW] * o[P_CV_COUT] * o[P_CV_R] * o[P_CV_S] * \
-                o[P_CV_CIN]
+            cin = min(o[P_CV_CIN], true_c.get(o[P_CV_IN], o[P_CV_CIN]))   # stem: 3 of 8
+            total += 2 * o[P_CV_OH] * o[P_CV_OW] * o[P_CV_COUT] * o[P_CV_R] * o[P_CV_S] * cin
         elif o.kind == OP_LINEAR:
             total += 2 * o[P_LN_ROWS] * o[P_LN_N] * o[P_LN_K]
         elif o.kind == OP_DWCONV:

@@ -47,6 +47,7 @@ def _declare(lib):
         "b2_profile_ops": (c.c_int, [P, c.c_int, c.c_int, c.POINTER(c.c_float),
                                      c.POINTER(c.c_int), c.POINTER(c.c_int)]),
         "b2_read_tensor": (c.c_int, [P, c.c_int, c.c_int, P, c.c_size_t]),
+        "b2_plan_memory": (c.c_int, [P, c.POINTER(c.c_uint64)]),
         "b2_plan_destroy": (None, [P]),
         "b2_last_error": (c.c_char_p, []),
         "b2_version": (c.c_char_p, []),
@@ -60,7 +61,7 @@ def _declare(lib):
 
 EXPORTED = ("b2_plan_create", "b2_plan_io", "b2_plan_info", "b2_forward", "b2_forward_host",
             "b2_bench", "b2_bench_e2e", "b2_gen_input", "b2_profile_ops", "b2_read_tensor",
-            "b2_plan_destroy",
+            "b2_plan_memory", "b2_plan_destroy",
             "b2_last_error", "b2_version")
 
 
@@ -171,11 +172,14 @@ class Plan:
             _raise(rc, "bench")
         return lat, comp
 
-    def read_tensor(self, batch: int, tensor: int, elems: int, kind: int) -> np.ndarray:
+    def read_tensor(self, batch: int, tensor: int, elems: int, kind: int,
+                    rows=None) -> np.ndarray:
         """Activation `tensor` of the last forward at `batch`, as float64 (or
         int32 ids) — the verification hook used by the layerwise parity tests.
         None when the executor fused the tensor into its consumer (never
-        materialised, e.g. the stem output under the fused stem/max-pool)."""
+        materialised, e.g. the stem output under the fused stem/max-pool).
+        ``rows``: keep only these samples (converted after the slice, so a
+        batch-256 activation is never widened to float64 whole)."""
         if kind == 1:
             buf = np.empty(batch * elems, dtype=np.int32)
         elif self.dtype == DT_BF16:
@@ -187,9 +191,19 @@ class Plan:
             return None
         if rc != B2_OK:
             _raise(rc, "read_tensor")
+        if rows is not None:
+            buf = buf.reshape(batch, elems)[list(rows)].reshape(-1)
         if buf.dtype == np.uint16:
             return (buf.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
         return buf.astype(np.float64) if kind != 1 else buf
+
+    def device_bytes(self) -> int:
+        """Device memory held by the plan (b2_plan_memory)."""
+        v = ctypes.c_uint64()
+        rc = self._lib.b2_plan_memory(self._h, ctypes.byref(v))
+        if rc != B2_OK:
+            _raise(rc, "plan_memory")
+        return int(v.value)
 
     def profile_ops(self, batch: int, iters: int = 5) -> list[tuple[int, float]]:
         cap = 4096

@@ -38,16 +38,25 @@ def read_exact(sock: socket.socket, n: int) -> bytes | None:
 
 
 def read_frame(sock: socket.socket) -> bytes | None:
+    """One length-prefixed frame.  Limits are enforced before the body is
+    buffered: a frame over 64 MiB must announce itself as binary (its first
+    4 body bytes are B2BN) or it is rejected from the header alone, like the
+    reference's MAX_FRAME check (mockserve/server.py:35,191-196)."""
     head = read_exact(sock, 4)
     if head is None:
         return None
     (length,) = _LEN.unpack(head)
     if length > MAX_BIN_FRAME:
         raise ValueError(f"frame of {length} bytes exceeds limit")
-    body = read_exact(sock, length)
-    if body is not None and length > MAX_JSON_FRAME and not body.startswith(BIN_MAGIC):
+    if length <= MAX_JSON_FRAME:
+        return read_exact(sock, length)
+    magic = read_exact(sock, 4)
+    if magic is None:
+        return None
+    if magic != BIN_MAGIC:
         raise ValueError(f"JSON frame of {length} bytes exceeds limit")
-    return body
+    rest = read_exact(sock, length - 4)
+    return None if rest is None else magic + rest
 
 
 def write_frame(sock: socket.socket, payload: bytes) -> None:

@@ -16,7 +16,18 @@ __main__.py:18-60, server.py:91-241) behind the same process contract:
 
 ``predict`` runs the real forward (libb2 ``b2_forward_host``) instead of
 sleeping; ``service_ms`` is the measured device-side request time.  ``bench``
-runs a sweep cell's closed loop on the device (libb2 ``b2_bench``).
+runs a sweep cell's closed loop on the device (libb2 ``b2_bench``) and
+returns, with the LatencySamples fields, the cell's own resource trace: per
+request the share of device time the forward kept the GPU busy (CUDA-event
+latency over the completion interval) and the plan's device memory
+(``b2_plan_memory``) — what the reference's ``_ResourceTrace`` samples for a
+CPU instance (profiler/sweep.py:51-79), but timed on the device and confined
+to the cell.
+
+Reference flags kept: ``--fault-script`` (``<t_ms> health_fail|health_ok``
+lines, mockserve/server.py:59-88, __main__.py:26,44) and ``--ready-delay-ms``.
+New: ``--max-batch N [--batch-timeout-ms T]`` merges concurrent predict
+requests into one forward (online.DynamicBatcher).
 """
 
 from __future__ import annotations
@@ -58,17 +69,55 @@ def load_plan(data: bytes) -> tuple[bytes, dict]:
     return data, P.decode(data, verify_crc=False).meta
 
 
+class FaultScript:
+    """Timed health flips: lines of ``<t_ms> health_fail|health_ok``; the state
+    at time t is the last action whose timestamp has passed (the reference's
+    FaultScript, mockserve/server.py:59-88)."""
+
+    ACTIONS = {"health_fail": False, "health_ok": True}
+
+    def __init__(self, events: list[tuple[float, str]]):
+        for _, action in events:
+            if action not in self.ACTIONS:
+                raise ValueError(f"unknown fault action '{action}'")
+        self.events = sorted(events)
+
+    @classmethod
+    def from_file(cls, path) -> "FaultScript":
+        events = []
+        for line in Path(path).read_text().splitlines():
+            line = line.strip()
+            if line and not line.startswith("#"):
+                t_ms, action = line.split()
+                events.append((float(t_ms), action))
+        return cls(events)
+
+    def healthy_at(self, elapsed_ms: float) -> bool:
+        ok = True
+        for t_ms, action in self.events:
+            if t_ms <= elapsed_ms:
+                ok = self.ACTIONS[action]
+        return ok
+
+
 class Executor:
     """Model behaviour shared by both protocols (the MockServer analogue)."""
 
-    def __init__(self, plan_bytes: bytes, dtype: int, meta: dict | None = None):
+    def __init__(self, plan_bytes: bytes, dtype: int, meta: dict | None = None,
+                 fault_script: FaultScript | None = None, max_batch: int = 0,
+                 batch_timeout_ms: float = 2.0):
         from .runtime import Plan
         self.plan = Plan(plan_bytes, dtype)
         self.meta = meta if meta is not None else P.decode(plan_bytes).meta
+        self.fault_script = fault_script or FaultScript([])
         self.started = time.monotonic()
+        self.batcher = None
+        if max_batch > 0:
+            from .online import DynamicBatcher
+            self.batcher = DynamicBatcher(self.plan.predict, max_batch, batch_timeout_ms)
 
     def healthy(self) -> bool:
-        return True
+        return self.fault_script.healthy_at((time.monotonic() - self.started) * 1000.0)
 
     def info(self) -> dict:
         p = self.plan
@@ -78,6 +127,9 @@ class Executor:
                 "model": self.meta.get("model", "")}
 
     def predict_array(self, x: np.ndarray) -> tuple[np.ndarray, float]:
+        if self.batcher is not None:
+            out, ms, _ = self.batcher.submit(x)
+            return out, ms
         t0 = time.perf_counter()
         out = self.plan.predict(x)
         return out, (time.perf_counter() - t0) * 1000.0
@@ -99,8 +151,13 @@ class Executor:
         if batch < 1 or n < 1:
             raise ValueError("batch and n must be >= 1")
         lat, comp = self.plan.bench(batch, n, warm, seed, e2e=bool(req.get("e2e", False)))
+        mem = self.plan.device_bytes()
+        prev = np.concatenate([[0.0], comp[:-1]])
+        busy = np.clip(lat / np.maximum(comp - prev, 1e-9), 0.0, 1.0)
         return {"ok": True, "batch": batch, "latencies_ms": lat.tolist(),
-                "completions_ms": comp.tolist()}
+                "completions_ms": comp.tolist(),
+                "resource_trace": [[float(t), float(b), mem] for t, b in zip(comp, busy)],
+                "device_bytes": mem}
 
 
 class _RestServer(ThreadingHTTPServer):
@@ -129,7 +186,10 @@ class _RestHandler(BaseHTTPRequestHandler):
 
     def do_GET(self):
         if self.path == "/health":
-            self._send(200, {"status": "ok"})
+            if self.server.ex.healthy():
+                self._send(200, {"status": "ok"})
+            else:
+                self._send(503, {"status": "unhealthy"})
         else:
             self._send(404, {"error": "not found"})
 
@@ -195,7 +255,8 @@ class _FrameHandler(socketserver.BaseRequestHandler):
         msg = json.loads(raw)
         kind = msg.get("kind")
         if kind == "health":
-            reply = {"ok": True, "status": "ok"}
+            ok = ex.healthy()
+            reply = {"ok": ok, "status": "ok" if ok else "unhealthy"}
         elif kind == "predict":
             reply = dict(ex.predict(msg.get("inputs")), ok=True)
         elif kind == "bench":
@@ -222,6 +283,13 @@ def build_parser() -> argparse.ArgumentParser:
     ap.add_argument("--host", default="127.0.0.1")
     ap.add_argument("--dtype", choices=["auto", "bf16", "fp32"], default="auto",
                     help="execution dtype (auto: the plan header's)")
+    ap.add_argument("--fault-script", default=None, help="file of '<t_ms> <action>' lines")
+    ap.add_argument("--ready-delay-ms", type=float, default=0.0,
+                    help="artificial delay before announcing readiness (for tests)")
+    ap.add_argument("--max-batch", type=int, default=0,
+                    help="dynamic batching: merge concurrent predicts up to this many samples")
+    ap.add_argument("--batch-timeout-ms", type=float, default=2.0,
+                    help="dynamic batching: how long the first request waits for company")
     return ap
 
 
@@ -242,7 +310,13 @@ def main(argv=None) -> int:
         return FORMAT_EXIT
     dtype = {"auto": -1, "bf16": P.DT_BF16, "fp32": P.DT_FP32}[args.dtype]
     try:
-        ex = Executor(plan_bytes, dtype, meta)
+        fault = FaultScript.from_file(args.fault_script) if args.fault_script else None
+    except (ValueError, OSError) as exc:
+        print(f"cannot start: {exc}", file=sys.stderr)
+        return FORMAT_EXIT
+    try:
+        ex = Executor(plan_bytes, dtype, meta, fault_script=fault, max_batch=args.max_batch,
+                      batch_timeout_ms=args.batch_timeout_ms)
     except PlanFormatError as exc:
         print(f"cannot load plan: {exc}", file=sys.stderr)
         return FORMAT_EXIT
@@ -254,6 +328,8 @@ def main(argv=None) -> int:
         print(f"worker start: read {t_read - t_start:.3f} s, decode {t_dec - t_read:.3f} s, "
               f"plan create {t_ready - t_dec:.3f} s", file=sys.stderr)
     server = serve(ex, args.protocol, args.host)
+    if args.ready_delay_ms > 0:
+        time.sleep(args.ready_delay_ms / 1000.0)
     # SIGTERM ends the process at once: the driver reclaims the CUDA context
     # and device memory.  A graceful interpreter shutdown (module teardown,
     # context destroy) took 2-3 s per worker, which the profiler's per-job

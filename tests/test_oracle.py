@@ -2,7 +2,7 @@
 
 * C1 MLP: against oracle/toyref.c (independent C fp64 restatement over the
   reference's toy-binary bytes) and tests/golden/mlp_golden.json;
-* ResNet-50 / MobileNetV2 / BERT-base: against the torchvision / transformers
+* ResNet-50 / MobileNetV2 / VGG-16 / BERT-base: against the torchvision / transformers
   modules' own fp64 CPU forward (third-party, not in /root/reference; parity
   of the converter's BN folding, OHWI layouts, QKV fusion and flatten order).
 * the device input generator's CPU restatement (oracle/gen_ref.py) sanity.
@@ -20,6 +20,8 @@ import toyref
 from paper_2006_05096_b200 import plan as P
 from paper_2006_05096_b200 import toyformat, zoo
 
+# 2 * MACs of torchvision vgg16 at 224x224 (13 convs + 3 linears; 30.941 GFLOP)
+VGG16_FLOPS = 30940528640
 GOLD = json.loads((Path(__file__).parent / "golden" / "mlp_golden.json").read_text())
 
 
@@ -42,7 +44,7 @@ def test_toyref_rejects_corruption():
         toyref.forward(bytes(blob), np.zeros((1, 784)))
 
 
-@pytest.mark.parametrize("name", ["resnet50", "mobilenet_v2", "bert"])
+@pytest.mark.parametrize("name", ["resnet50", "mobilenet_v2", "vgg16", "bert"])
 def test_oracle_matches_framework_forward(name):
     import torch
     torch.set_num_threads(8)
@@ -60,7 +62,7 @@ def test_oracle_matches_framework_forward(name):
     # only the plan's fp32 weight storage separates the two
     assert plan_ref.normwise_err(out, ref) < 2e-5
     assert pl.meta["flops_per_sample"] == {"resnet50": 8178368512, "mobilenet_v2": 601548544,
-                                           "bert": 22348431360}[name]
+                                           "vgg16": VGG16_FLOPS, "bert": 22348431360}[name]
 
 
 def test_bf16_emulation_is_round_to_nearest_even():

@@ -54,3 +54,14 @@ def test_norm_and_gelu_lowering():
     pl = P.decode(zoo.emit_toy(g).build())
     assert [o.kind for o in pl.ops] == [P.OP_INPUT, P.OP_LINEAR, P.OP_LAYERNORM, P.OP_ACT,
                                         P.OP_OUTPUT]
+
+
+@pytest.mark.parametrize("name,flops", [("resnet50", 8178368512), ("mobilenet_v2", 601548544),
+                                        ("bert", 22348431360), ("vgg16", 30940528640),
+                                        ("mlp", 406528)])
+def test_flops_count_true_channels(name, flops):
+    """Algorithmic FLOPs use the model's true channels (the 3-channel stem is
+    padded to 8 in the plan; the padding is not work) — the roofline numerator
+    (SURVEY.md §8(d)); libb2's b2_plan_info applies the same rule."""
+    pl = P.decode(zoo.build_plan(name, P.DT_BF16, seed=0))
+    assert P.flops_per_sample(pl) == pl.meta["flops_per_sample"] == flops

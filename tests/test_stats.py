@@ -85,9 +85,20 @@ def test_monotone_in_p(samples, a, b):
     assert percentile(samples, lo) <= percentile(samples, hi)
 
 
-def test_merged_shards_union():
-    a = LatencySamples([1.0, 2.0], [1.0, 3.0])
-    b = LatencySamples([3.0], [2.0], failed=1)
-    m = a.merged(b)
-    assert sorted(m.latencies_ms) == [1.0, 2.0, 3.0] and m.completions_ms == [1.0, 2.0, 3.0]
-    assert m.failed == 1
+def test_sharded_cell_union_latency_and_max_peak():
+    """A request-sharded cell: latencies are the union of the shards', peak
+    throughput the max of the per-shard peaks (never the pooled completions,
+    which would report k GPUs' combined rate)."""
+    from paper_2006_05096_b200.profiler.stats import ShardedSamples, peak_throughput
+    a = LatencySamples([10.0] * 50, [10.0 * (i + 1) for i in range(50)])          # 100 req/s
+    b = LatencySamples([12.0] * 50, [12.0 * (i + 1) for i in range(50)], failed=1)
+    sh = ShardedSamples([a, b])
+    u = sh.union()
+    assert sorted(u.latencies_ms) == sorted(a.latencies_ms + b.latencies_ms) and u.failed == 1
+    assert sh.peak_throughput(4) == max(peak_throughput(a.completions_ms, 4),
+                                        peak_throughput(b.completions_ms, 4)) == 400.0
+    pooled = peak_throughput(sorted(a.completions_ms + b.completions_ms), 4)
+    assert pooled > 600.0                       # what naive pooling would claim
+    r = aggregate(sh, [], 4, variant_id="v", device="gpu:0", backend="b200", protocol="rest")
+    assert r.peak_throughput == 400.0 and r.raw_sample_count == 100
+    assert r.p99_latency_ms == 12.0 and r.p50_latency_ms == 10.0

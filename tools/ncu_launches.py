@@ -34,7 +34,7 @@ head = (f"one ResNet-50 bf16 batch-256 forward from the ncu launch list (cold ca
         f"compare shares, not absolutes)\ntotal {tot:.1f} us over {len(fwd)} launches; "
         f"tcgen05 conv/GEMM share {100 * share:.1f}%, avg DRAM traffic per launch {tb / 1e6:.1f} MB\n")
 open(out_summary, 'w').write(head + "\n".join(lines) + "\n")
-json.dump({"tcgen05_bytes_per_launch": tb, "tcgen05_launches_per_forward": len(tc),
+json.dump({"model": "resnet50", "batch": 256, "tcgen05_bytes_per_launch": tb, "tcgen05_launches_per_forward": len(tc),
            "tcgen05_time_share_ncu": share, "family": list(FAMILY), "forward_us_ncu": tot,
            "source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
                      "--clock-control none, python bench.py --steps 2 --warmup 3 --no-sweep --no-cpu"},
