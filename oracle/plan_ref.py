@@ -289,7 +289,13 @@ def op_io(o):
     return [o[0]], o[1]
 
 
-def layerwise_errors(plan, read_tensor, x, emulate_bf16: bool):
+# Layerwise teacher-forced bound for bf16 kernels (tests): one round-to-nearest
+# of the op output is <= u = 2^-8 = 3.91e-3 normwise; +15% for fp32
+# accumulation order and near-tie elements.  An fp32 kernel: 1e-5.
+BF16_LAYERWISE_TOL = 4.5e-3
+
+
+def layerwise_errors(plan, read_tensor, x, emulate_bf16: bool, roundings=None):
     """Teacher-forced per-op parity.
 
     Every op is recomputed on the host from the executor's OWN input tensors
@@ -302,8 +308,21 @@ def layerwise_errors(plan, read_tensor, x, emulate_bf16: bool):
     The reference value of each op is its EXACT (float64) result on the
     executor's bf16 inputs and bf16 weights, not rounded to bf16: a correct
     bf16 kernel then differs from it by one round-to-nearest of its output
-    (<= 2^-9 of the element, so <= 1.95e-3 normwise) plus its fp32
-    accumulation error.  Per-sample ops only, so ``x`` and ``read_tensor`` may
+    (bf16 keeps 8 significant bits: <= 2^-8 of the element's binade, so
+    <= u = 2^-8 = 3.91e-3 normwise) plus its fp32 accumulation error.
+    Tensors the executor never materialises are teacher-forced from the
+    oracle: rounded to bf16 where the kernel holds them as bf16 on chip (the
+    stem's output before the fused max-pool), exact where the kernel folds
+    them into an fp32 accumulator (a projection shortcut consumed only as
+    the residual of the block's last conv: its K blocks are appended to that
+    conv's GEMM, so it is never rounded).
+
+    ``roundings`` (a dict, optional) receives, per op index, how many bf16
+    roundings separate the exact value from the kernel's output: 1 for most
+    ops; 2 for attention (P = softmax(QK^T) is rounded to bf16 before PV) and
+    for ops fed by a tensor the kernel rounds on chip (kernel and oracle round
+    the same fp32/exact value and can land one ulp apart at near-ties).  A
+    test's bound is BF16_LAYERWISE_TOL x roundings.  Per-sample ops only, so ``x`` and ``read_tensor`` may
     be restricted to a subset of the batch rows (the full-size parity tests
     check rows 0, B/2-1 and B-1 of a batch-256 forward).
     """
@@ -319,6 +338,19 @@ def layerwise_errors(plan, read_tensor, x, emulate_bf16: bool):
     out = np.zeros((B, plan.out_elems))
     res = []
     oracle_t = {}   # oracle values of tensors the executor fused away (never materialised)
+    consumers: dict = {}
+    for o in plan.ops:
+        if o.kind == P.OP_CONV:
+            consumers.setdefault(o[P.P_CV_IN], []).append("in")
+            if o[P.P_CV_RES] >= 0:
+                consumers.setdefault(o[P.P_CV_RES], []).append("res")
+        elif o.kind == P.OP_LINEAR:
+            consumers.setdefault(o[P.P_LN_IN], []).append("in")
+            if o[P.P_LN_RES] >= 0:
+                consumers.setdefault(o[P.P_LN_RES], []).append("res")
+        else:
+            for t in op_io(o)[0]:
+                consumers.setdefault(t, []).append("in")
     for i, o in enumerate(plan.ops):
         ins, dst = op_io(o)
         if dst is None:
@@ -332,13 +364,29 @@ def layerwise_errors(plan, read_tensor, x, emulate_bf16: bool):
                 dict.__setitem__(T, t, np.asarray(v, dtype=np.int64).reshape(B, -1))
             else:
                 dict.__setitem__(T, t, np.asarray(v, dtype=np.float64))
+        if roundings is not None:
+            fed = any(t in oracle_t and emulate_bf16 and not
+                      (consumers.get(t) and all(c == "res" for c in consumers[t])) for t in ins)
+            roundings[i] = 2 if (o.kind == P.OP_ATTENTION or fed) else 1
         run_op(plan, o, T, W, B, x, out, np.float64)
         ref = np.asarray(T[dst], dtype=np.float64).reshape(B, -1)
         got = read_tensor(dst)
         if got is None:
-            # the kernel holds fused intermediates as bf16 (on chip) too
-            oracle_t[dst] = round_bf16(ref).astype(np.float64) if emulate_bf16 else ref
+            folded = consumers.get(dst) and all(c == "res" for c in consumers[dst])
+            oracle_t[dst] = round_bf16(ref).astype(np.float64) \
+                if emulate_bf16 and not folded else ref
             continue
         got = np.asarray(got, dtype=np.float64).reshape(B, -1)
         res.append((i, o.name, normwise_err(got, ref)))
     return res
+
+
+def layerwise_check(plan, read_tensor, x, emulate_bf16: bool):
+    """layerwise_errors with each op's bound: [(op, name, err, bound)] and the
+    ops over it.  bf16: BF16_LAYERWISE_TOL x the op's bf16 roundings; fp32:
+    1e-5."""
+    rnd: dict = {}
+    res = layerwise_errors(plan, read_tensor, x, emulate_bf16, roundings=rnd)
+    out = [(i, n, e, (BF16_LAYERWISE_TOL * rnd.get(i, 1)) if emulate_bf16 else 1e-5)
+           for i, n, e in res]
+    return out, [r for r in out if not r[2] <= r[3]]

@@ -5,7 +5,8 @@ Parity is checked three ways, all through the C ABI (libb2):
   bf16: 2e-2 vs fp32 where the model is well conditioned — MLP, BERT);
 * layerwise, teacher-forced: every op recomputed by the oracle from the
   executor's own input tensors (b2_read_tensor), bound = one rounding of the
-  op output (bf16 1e-2 normwise ~ 2.5 ulp, fp32 1e-5) — the gate for the deep
+  op output (bf16 plan_ref.BF16_LAYERWISE_TOL = 4.5e-3 normwise, one rounding
+  u = 2^-8 + 15%; fp32 1e-5) — the gate for the deep
   random CNNs, whose end-to-end bf16 error is dominated by their own chaos
   (DESIGN.md §4: a 2^-9 input perturbation moves ResNet-50 logits by 6%);
 * size-independent properties at the benchmark size (b=256): batch
@@ -55,9 +56,7 @@ def test_parity(gpu_required, name, dtype):
         else:
             assert err <= 0.25, err      # sanity only; the layerwise check is the gate
         rt = lambda t: plan.read_tensor(B, t, pl.tensors[t].elems, pl.tensors[t].kind)
-        tol = 1e-2 if dtype == P.DT_BF16 else 1e-5
-        bad = [r for r in plan_ref.layerwise_errors(pl, rt, x, dtype == P.DT_BF16)
-               if not r[2] <= tol]
+        _, bad = plan_ref.layerwise_check(pl, rt, x, dtype == P.DT_BF16)
         assert not bad, bad[:5]
     finally:
         plan.close()

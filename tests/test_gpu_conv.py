@@ -2,8 +2,9 @@
 conv path (banded implicit GEMM with resident or streamed weights and 1..4 M
 tiles per band, the TMA-im2col GEMM, the space-to-depth stem) checked
 layerwise against the numpy oracle (plan_ref.conv2d_nhwc on the bf16-rounded
-operands, fp64 accumulation).  Tolerance: 1e-2 normwise = one bf16 rounding
-of the op output (same bound as tests/test_gpu.py's layerwise gate).
+operands, fp64 accumulation).  Tolerance: plan_ref.BF16_LAYERWISE_TOL
+(4.5e-3 normwise = one bf16 rounding of the op output, u = 2^-8, + 15%; the
+same bound as tests/test_gpu.py's layerwise gate).
 
 Batch sizes are chosen so both the small-batch (one M tile per band) and the
 large-batch (multi-tile bands) configurations run for each shape.
@@ -17,7 +18,7 @@ from paper_2006_05096_b200 import runtime as R
 
 pytestmark = pytest.mark.gpu
 
-TOL = 1e-2
+TOL = plan_ref.BF16_LAYERWISE_TOL
 
 
 def conv_plan(H, W, C, N, k, stride, act=1, seed=0):
@@ -49,8 +50,7 @@ def check(blob, batch, seed=3):
         out = plan.predict(x)
         assert np.isfinite(out).all()
         rt = lambda t: plan.read_tensor(batch, t, pl.tensors[t].elems, pl.tensors[t].kind)
-        errs = plan_ref.layerwise_errors(pl, rt, x, True)
-        bad = [e for e in errs if not e[2] <= TOL]
+        errs, bad = plan_ref.layerwise_check(pl, rt, x, True)
         assert not bad, bad
     finally:
         plan.close()
@@ -132,8 +132,8 @@ def test_stem_maxpool(gpu_required, monkeypatch, batch, fused):
         assert np.isfinite(out).all()
         rt = lambda t: plan.read_tensor(batch, t, pl.tensors[t].elems, pl.tensors[t].kind)
         assert (rt(pl.ops[1][1]) is None) == (fused == "1")
-        errs = plan_ref.layerwise_errors(pl, rt, x, True)
-        assert errs and all(e[2] <= TOL for e in errs), errs
+        errs, bad = plan_ref.layerwise_check(pl, rt, x, True)
+        assert errs and not bad, errs
     finally:
         plan.close()
 
@@ -233,8 +233,8 @@ def test_shortcut_fold(gpu_required, monkeypatch, H, C, Cm, N, stride, batch, fo
         assert np.isfinite(out).all()
         rt = lambda t: plan.read_tensor(batch, t, pl.tensors[t].elems, pl.tensors[t].kind)
         assert (rt(pl.ops[2][1]) is None) == (fold == "1")
-        errs = plan_ref.layerwise_errors(pl, rt, x, True)
-        assert errs and all(e[2] <= TOL for e in errs), errs
+        errs, bad = plan_ref.layerwise_check(pl, rt, x, True)
+        assert errs and not bad, errs
     finally:
         plan.close()
 
@@ -449,7 +449,7 @@ def test_band_maxpool2(gpu_required, monkeypatch, H, W, C, N, batch, fused):
         assert np.isfinite(out).all()
         rt = lambda t: plan.read_tensor(batch, t, pl.tensors[t].elems, pl.tensors[t].kind)
         assert (rt(pl.ops[1][1]) is None) == (fused == "1")
-        errs = plan_ref.layerwise_errors(pl, rt, x, True)
-        assert errs and all(e[2] <= TOL for e in errs), errs
+        errs, bad = plan_ref.layerwise_check(pl, rt, x, True)
+        assert errs and not bad, errs
     finally:
         plan.close()

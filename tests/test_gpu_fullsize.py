@@ -10,10 +10,15 @@ executor's own bf16 inputs and compared with its bf16 output.  All ops are
 per-sample, so the host recomputation runs on three sampled rows of the batch
 (first, middle, last) read back from the batch-256 activations.
 
-Tolerance: 4e-3 normwise (max|got-exact| / max|exact|).  One round-to-nearest
-of a bf16 output is <= 2^-9 = 1.95e-3 of the element; the remainder covers the
-fp32 accumulation-order difference.  The worst margin per model is printed
-and, with B2_PARITY_LOG=<path>, written as JSON (profiles/ keeps a copy).
+Tolerance: per op, 4.5e-3 normwise (max|got-exact| / max|exact|) per bf16
+rounding.  One round-to-nearest of a bf16 output is <= u = 2^-8 = 3.91e-3 of the largest element's
+binade (bf16 keeps 8 significant bits); the remaining 15% covers the fp32
+accumulation-order difference.  Ops with a second rounding get twice that
+(plan_ref.layerwise_check): attention (P is rounded to bf16 before PV) and
+ops fed by a tensor the kernel keeps on chip as bf16 (the stem before its
+fused max-pool, VGG's conv before its fused 2x2 pool) — kernel and oracle
+round the same value once each and can land one ulp apart at near-ties.
+The worst margin per model is printed and, with B2_PARITY_LOG=<path>, written as JSON (profiles/ keeps a copy).
 """
 import json
 import os
@@ -28,7 +33,7 @@ from paper_2006_05096_b200 import zoo
 
 pytestmark = pytest.mark.gpu
 
-BF16_LAYERWISE_TOL = 4e-3
+BF16_LAYERWISE_TOL = plan_ref.BF16_LAYERWISE_TOL
 FULL = [("resnet50", 256), ("bert", 128), ("vgg16", 256), ("mobilenet_v2", 256)]
 
 
@@ -48,7 +53,7 @@ def _log(entry: dict):
 
 
 def sampled_layerwise(plan, pl, x, rows):
-    """layerwise_errors over `rows` of a full-batch forward already run on x."""
+    """layerwise_check over `rows` of a full-batch forward already run on x."""
     B = x.shape[0]
     cache = {}
 
@@ -57,7 +62,7 @@ def sampled_layerwise(plan, pl, x, rows):
             cache[t] = plan.read_tensor(B, t, pl.tensors[t].elems, pl.tensors[t].kind, rows=rows)
         return cache[t]
 
-    return plan_ref.layerwise_errors(pl, rt, x[rows], True)
+    return plan_ref.layerwise_check(pl, rt, x[rows], True)
 
 
 @pytest.mark.parametrize("name,batch", FULL)
@@ -71,17 +76,15 @@ def test_layerwise_parity_at_timed_config(gpu_required, name, batch):
         y = plan.predict(x)
         assert np.isfinite(y).all()
         rows = [0, batch // 2 - 1, batch - 1]
-        res = sampled_layerwise(plan, pl, x, rows)
+        res, bad = sampled_layerwise(plan, pl, x, rows)
         assert len(res) >= len([o for o in pl.ops if o.kind in (P.OP_CONV, P.OP_LINEAR)]) // 2
-        worst = max(res, key=lambda r: r[2])
+        worst = max(res, key=lambda r: r[2] / r[3])
         print(f"\n{name} b={batch}: {len(res)} ops, worst {worst[2]:.3e} at op {worst[0]} "
-              f"({worst[1]}), tol {BF16_LAYERWISE_TOL:g}, margin "
-              f"{BF16_LAYERWISE_TOL / max(worst[2], 1e-30):.2f}x")
+              f"({worst[1]}), bound {worst[3]:g}, margin {worst[3] / max(worst[2], 1e-30):.2f}x")
         _log({"case": f"{name}_b{batch}_bf16", "ops": len(res), "rows": rows,
-              "tol": BF16_LAYERWISE_TOL, "worst": worst[2], "worst_op": worst[1],
-              "median": float(np.median([r[2] for r in res])),
-              "per_op": [[i, n, round(e, 6)] for i, n, e in res]})
-        bad = [r for r in res if not r[2] <= BF16_LAYERWISE_TOL]
+              "tol_one_rounding": BF16_LAYERWISE_TOL, "worst": worst[2], "worst_op": worst[1],
+              "worst_bound": worst[3], "median": float(np.median([r[2] for r in res])),
+              "per_op": [[i, n, round(e, 6), b] for i, n, e, b in res]})
         assert not bad, bad[:5]
     finally:
         plan.close()

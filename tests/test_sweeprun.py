@@ -120,3 +120,58 @@ def test_sharded_sweep_gloo_world_size_2():
         p.join(timeout=60)
     assert len(got) == 45 and len({(v, b) for v, b, _ in got}) == 45
     assert {d for _, _, d in got} == {"gpu:0", "gpu:1"}
+
+
+def _partitioned_main(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_2006_05096_b200.profiler.stats import LatencySamples
+    from paper_2006_05096_b200.sweeprun import partitioned_sweep
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    jobs = [ProfilingJob(m, "r" + m, "v" + m,
+                         SweepSpec(batch_sizes=BATCHES, devices=["gpu:*"], backends=["b200"],
+                                   protocols=["grpc-style"], requests_per_cell=100,
+                                   warmup_requests=10)) for m in MODELS]
+    cost = lambda j, c: cell_cost(MODELS[j.id], c, c.shard_requests(100), 10)
+    measured = []
+
+    def measure(job, unit):
+        measured.append(job.id + ":" + unit.key())
+        n = unit.shard_requests(job.sweep.requests_per_cell)
+        lat = 1.0 + unit.shard
+        return LatencySamples([lat] * n, [lat * (i + 1) for i in range(n)])
+
+    res = partitioned_sweep(jobs, rank, world, measure, cost, setup_s=lambda j: 0.5)
+    q.put((rank, measured, [(r.variant_id, r.batch_size, r.device, r.raw_sample_count,
+                             r.peak_throughput) for r in res]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_partitioned_sweep_with_request_shards_gloo(world):
+    """world_size 2 and 4 on gloo: heavy cells are request-sharded across
+    ranks, every unit is measured exactly once, rank 0 folds 45 results
+    with each sharded cell's 100 requests and max-of-shards peak."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + world + os.getpid() % 500
+    procs = [ctx.Process(target=_partitioned_main, args=(r, world, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    units = [u for _, m, _ in got for u in m]
+    assert len(units) == len(set(units))                      # each unit measured once
+    # ideal per-rank load at world 4 is below 2x VGG-16 b=256: that cell is
+    # split; at world 2 no cell bounds the makespan and none is
+    assert any("#" in u for u in units) == (world == 4)
+    assert {r for r, m, _ in got if m} == set(range(world))   # every rank worked
+    res = next(r for rank, _, r in got if rank == 0)
+    assert len(res) == 45 and len({(v, b) for v, b, *_ in res}) == 45
+    assert all(n == 100 for *_, n, _ in res)
+    sharded = [r for r in res if "," in r[2]]
+    assert bool(sharded) == (world == 4) and all(pk == pytest.approx(r[1] * 1000.0) for r in sharded
+                           for pk in [r[4]])                  # shard 0's 1 ms/request
