@@ -33,3 +33,13 @@ def normal(n, seed):
 def tokens(n, vocab, seed):
     h = _hash(n, seed)
     return (((h >> np.uint64(32)) * np.uint64(vocab)) >> np.uint64(32)).astype(np.int64)
+
+
+def plan_tokens(batch, seq, vocab, seed, masked):
+    """The token input b2_gen_input writes for a plan: per sample [ids(seq)]
+    or, for attention-mask plans, [ids(seq), ones(seq)]; id j of sample b is
+    stream element b * seq + j either way (kernels.cu gen_tokens_kernel)."""
+    ids = tokens(batch * seq, vocab, seed).reshape(batch, seq)
+    if not masked:
+        return ids.reshape(-1)
+    return np.concatenate([ids, np.ones((batch, seq), np.int64)], 1).reshape(-1)

@@ -109,16 +109,40 @@ def layernorm(x, g, b, eps):
     return (x - mu) / np.sqrt(var + eps) * g + b
 
 
-def attention(qkv, heads, dh):
-    """qkv [B,S,3*H*Dh] -> [B,S,H*Dh]; softmax(QK^T/sqrt(Dh)) V, no mask."""
+def attention(qkv, heads, dh, keymask=None):
+    """qkv [B,S,3*H*Dh] -> [B,S,H*Dh]; softmax(QK^T/sqrt(Dh) + bias) V with
+    bias = float32-min on padded keys (``keymask`` [B,S] bool, True = attend;
+    transformers' extended attention mask: modeling_bert's
+    get_extended_attention_mask, (1 - mask) * finfo.min), 0 elsewhere."""
     B, S, _ = qkv.shape
     q, k, v = np.split(qkv.reshape(B, S, 3, heads, dh), 3, axis=2)
     q, k, v = (t[:, :, 0].transpose(0, 2, 1, 3) for t in (q, k, v))   # [B,H,S,Dh]
     sc = q @ k.transpose(0, 1, 3, 2) / math.sqrt(dh)
+    if keymask is not None:
+        bias = np.where(np.asarray(keymask, bool), 0.0, float(np.finfo(np.float32).min))
+        sc = sc + bias[:, None, None, :]
     sc = sc - sc.max(-1, keepdims=True)
     p = np.exp(sc)
     p /= p.sum(-1, keepdims=True)
     return (p @ v).transpose(0, 2, 1, 3).reshape(B, S, heads * dh)
+
+
+def pack_keymask(valid):
+    """[B,S] bool -> [B,(S+31)//32] int32 words, bit j%32 of word j//32 = key
+    j valid (the TOKENS op's mask tensor, kernels.cu tokens_kernel)."""
+    valid = np.asarray(valid, bool)
+    B, S = valid.shape
+    nw = (S + 31) // 32
+    bits = np.zeros((B, nw * 32), bool)
+    bits[:, :S] = valid
+    w = (bits.reshape(B, nw, 32).astype(np.uint64) << np.arange(32, dtype=np.uint64)).sum(-1)
+    return w.astype(np.uint32).view(np.int32).astype(np.int64)
+
+
+def unpack_keymask(words, S):
+    w = np.asarray(words, dtype=np.int64).reshape(len(words), -1).astype(np.uint32)
+    bits = (w[:, :, None] >> np.arange(32, dtype=np.uint32)) & 1
+    return bits.reshape(len(w), -1)[:, :S].astype(bool)
 
 
 def round_bf16(x):
@@ -170,7 +194,11 @@ def run_op(plan, o, T, W, B, x, out, dtype=np.float64):
         buf[..., :C] = img
         T[o[P.P_IN_OUT]] = buf
     elif k == P.OP_TOKENS:
-        T[o[P.P_TK_OUT]] = np.asarray(x, dtype=np.int64).reshape(B, o[P.P_TK_SEQ])
+        S = o[P.P_TK_SEQ]
+        xi = np.asarray(x, dtype=np.int64).reshape(B, -1)
+        T[o[P.P_TK_OUT]] = xi[:, :S]
+        if o[P.P_TK_HASMASK]:
+            T[o[P.P_TK_MASK]] = pack_keymask(xi[:, S:2 * S] != 0)
     elif k == P.OP_CONV:
         y = conv2d_nhwc(shaped(o[P.P_CV_IN]), W[o[P.P_CV_W]], wt(o[P.P_CV_B]),
                         o[P.P_CV_STRIDE], o[P.P_CV_PAD])
@@ -212,7 +240,8 @@ def run_op(plan, o, T, W, B, x, out, dtype=np.float64):
                                      P.bits_f32(o[P.P_EM_EPS]))
     elif k == P.OP_ATTENTION:
         S, H, Dh = o[P.P_AT_SEQ], o[P.P_AT_HEADS], o[P.P_AT_DH]
-        T[o[P.P_AT_OUT]] = attention(T[o[P.P_AT_QKV]].reshape(B, S, 3 * H * Dh), H, Dh)
+        km = unpack_keymask(T[o[P.P_AT_MASK]], S) if o[P.P_AT_HASMASK] else None
+        T[o[P.P_AT_OUT]] = attention(T[o[P.P_AT_QKV]].reshape(B, S, 3 * H * Dh), H, Dh, km)
     elif k == P.OP_ACT:
         T[o[P.P_AC_OUT]] = _act(T[o[P.P_AC_IN]], o[P.P_AC_ACT])
     elif k == P.OP_OUTPUT:
@@ -261,8 +290,12 @@ def make_inputs(plan, batch: int, seed: int = 0):
         plan = P.decode(plan)
     rng = np.random.default_rng(seed)
     if plan.input_kind == P.IN_TOKENS:
-        vocab = next(o[P.P_TK_VOCAB] for o in plan.ops if o.kind == P.OP_TOKENS)
-        return rng.integers(0, vocab, size=(batch, plan.in_elems), dtype=np.int64)
+        tk = next(o for o in plan.ops if o.kind == P.OP_TOKENS)
+        S = tk[P.P_TK_SEQ]
+        ids = rng.integers(0, tk[P.P_TK_VOCAB], size=(batch, S), dtype=np.int64)
+        if tk[P.P_TK_HASMASK]:   # attention_mask = 1 (the profiling payload)
+            return np.concatenate([ids, np.ones((batch, S), np.int64)], 1)
+        return ids
     return rng.standard_normal((batch, plan.in_elems), dtype=np.float32)
 
 
@@ -278,6 +311,8 @@ def op_io(o):
     k = o.kind
     if k in (P.OP_INPUT, P.OP_TOKENS):
         return [], o[0]
+    if k == P.OP_ATTENTION and o[P.P_AT_HASMASK]:
+        return [o[P.P_AT_QKV], o[P.P_AT_MASK]], o[P.P_AT_OUT]
     if k == P.OP_CONV:
         return [o[P.P_CV_IN]] + ([o[P.P_CV_RES]] if o[P.P_CV_RES] >= 0 else []), o[P.P_CV_OUT]
     if k == P.OP_LINEAR:

@@ -4,7 +4,8 @@
 //   1. TMA brings Q, K, V (each 128 x 64 bf16, 128B-swizzled) straight out of
 //      the fused QKV activation [B*S, 3*H*64].
 //   2. S = Q K^T on the tensor core (M=128 queries, N=128 keys, K=64) into TMEM.
-//   3. Each thread owns one query row: tcgen05.ld its 128 scores, max /
+//   3. Each thread owns one query row: tcgen05.ld its 128 scores, padded
+//      keys (attention-mask bits, when given) replaced by float32 min, max /
 //      exp2 / sum in registers, writes unnormalised P (bf16) into smem in the
 //      K-major 128B-swizzled layout.
 //   4. O = P V (M=128, N=64, K=128; V consumed MN-major as stored) into TMEM.
@@ -51,7 +52,7 @@ B2_DEV void at_bar() { asm volatile("bar.sync 1, %0;" ::"n"(AT_WARPS * 32) : "me
 
 __global__ void __launch_bounds__(AT_WARPS * 32, AT_CTAS_PER_SM)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, bf16* __restrict__ out, int H,
-                   int units) {
+                   int units, const uint32_t* __restrict__ keymask) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -123,6 +124,15 @@ __global__ void __launch_bounds__(AT_WARPS * 32, AT_CTAS_PER_SM)
       for (int j = 0; j < 32; ++j) {
         sv[j] = __uint_as_float(r0[j]);
         sv[32 + j] = __uint_as_float(r1[j]);
+      }
+    }
+    if (keymask) {   // + float32 min on padded keys: exp2 of it underflows to 0
+      const int bq = u / H;
+      const uint32_t w0 = __ldg(keymask + bq * 4 + hh * 2), w1 = __ldg(keymask + bq * 4 + hh * 2 + 1);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (!((w0 >> j) & 1u)) sv[j] = -3.4028234663852886e38f;
+        if (!((w1 >> j) & 1u)) sv[32 + j] = -3.4028234663852886e38f;
       }
     }
     float mx = sv[0];
@@ -197,7 +207,8 @@ __global__ void __launch_bounds__(AT_WARPS * 32, AT_CTAS_PER_SM)
   }
 }
 
-cudaError_t attention_tc(const CUtensorMap& tm_qkv, bf16* out, int B, int H, cudaStream_t st) {
+cudaError_t attention_tc(const CUtensorMap& tm_qkv, bf16* out, int B, int H,
+                         const uint32_t* keymask, cudaStream_t st) {
   static bool cfg = false;
   if (!cfg) {
     cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel,
@@ -211,7 +222,7 @@ cudaError_t attention_tc(const CUtensorMap& tm_qkv, bf16* out, int B, int H, cud
   const int units = B * H;
   const int slots = AT_CTAS_PER_SM * sms;
   return launch_pdl(attn_tc_kernel, dim3(units < slots ? units : slots), dim3(AT_WARPS * 32),
-                    AT_SMEM, st, tm_qkv, out, H, units);
+                    AT_SMEM, st, tm_qkv, out, H, units, keymask);
 }
 
 }  // namespace b2

@@ -180,15 +180,36 @@ cudaError_t input_pack_s2d(const float* in, bf16* out, int B, int C, int H, int 
   return cudaGetLastError();
 }
 
-__global__ void tokens_kernel(const int64_t* in, int32_t* out, long n, int vocab) {
+__global__ void tokens_kernel(const int64_t* in, int32_t* out, long n, int S, int stride,
+                              int vocab) {
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  long v = in[i];
+  const long b = i / S, j = i - b * S;
+  long v = in[b * stride + j];
   v = v < 0 ? 0 : (v >= vocab ? vocab - 1 : v);
   out[i] = (int32_t)v;
 }
-cudaError_t tokens_pack(const int64_t* in, int32_t* out, long n, int vocab, cudaStream_t st) {
-  tokens_kernel<<<nblk(n, 256), 256, 0, st>>>(in, out, n, vocab);
+// attention_mask [S] int64 per sample (after the ids) -> key-validity bits:
+// one warp per 32 keys, bit l of the word = key (w * 32 + l) attends
+__global__ void keymask_kernel(const int64_t* in, uint32_t* out, int B, int S, int stride) {
+  const int nw = (S + 31) / 32;
+  const long wi = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wi >= (long)B * nw) return;
+  const long b = wi / nw;
+  const int key = (int)(wi - b * nw) * 32 + lane;
+  const bool valid = key < S && in[b * stride + S + key] != 0;
+  const uint32_t bits = __ballot_sync(0xffffffffu, valid);
+  if (lane == 0) out[wi] = bits;
+}
+cudaError_t tokens_pack(const int64_t* in, int32_t* out, uint32_t* mask, int B, int S,
+                        int stride, int vocab, cudaStream_t st) {
+  const long n = (long)B * S;
+  tokens_kernel<<<nblk(n, 256), 256, 0, st>>>(in, out, n, S, stride, vocab);
+  if (mask) {
+    const long warps = (long)B * ((S + 31) / 32);
+    keymask_kernel<<<nblk(warps * 32, 256), 256, 0, st>>>(in, mask, B, S, stride);
+  }
   return cudaGetLastError();
 }
 
@@ -1016,7 +1037,8 @@ cudaError_t embed_ln(const int32_t* ids, const T* word, const T* pos, const T* t
 // One CTA per (sample, head); K and V of the head staged in shared memory as
 // fp32; each thread owns query rows and runs a single-pass online softmax.
 template <typename T, int DH>
-__global__ void attention_kernel(const T* __restrict__ qkv, T* __restrict__ out, int S, int H) {
+__global__ void attention_kernel(const T* __restrict__ qkv, T* __restrict__ out, int S, int H,
+                                 const uint32_t* __restrict__ keymask) {
   extern __shared__ float kv[];
   float* Ks = kv;
   float* Vs = kv + S * DH;
@@ -1042,6 +1064,8 @@ __global__ void attention_kernel(const T* __restrict__ qkv, T* __restrict__ out,
       float sc = 0.f;
 #pragma unroll
       for (int d = 0; d < DH; ++d) sc = fmaf(q[d], Ks[j * DH + d], sc);
+      if (keymask && !((keymask[(long)b * ((S + 31) / 32) + (j >> 5)] >> (j & 31)) & 1u))
+        sc = -3.4028234663852886e38f;   // + float32 min (transformers' extended mask)
       if (sc > mx) {
         const float corr = __expf(mx - sc);
         sum *= corr;
@@ -1061,7 +1085,8 @@ __global__ void attention_kernel(const T* __restrict__ qkv, T* __restrict__ out,
   }
 }
 template <typename T>
-cudaError_t attention(const T* qkv, T* out, int B, int S, int H, int Dh, cudaStream_t st) {
+cudaError_t attention(const T* qkv, T* out, int B, int S, int H, int Dh,
+                      const uint32_t* keymask, cudaStream_t st) {
   if (Dh != 64) return cudaErrorInvalidValue;
   const size_t smem = (size_t)2 * S * 64 * sizeof(float);
   static bool cfg = false;
@@ -1070,7 +1095,7 @@ cudaError_t attention(const T* qkv, T* out, int B, int S, int H, int Dh, cudaStr
                          200 * 1024);
     cfg = true;
   }
-  attention_kernel<T, 64><<<B * H, 128, smem, st>>>(qkv, out, S, H);
+  attention_kernel<T, 64><<<B * H, 128, smem, st>>>(qkv, out, S, H, keymask);
   return cudaGetLastError();
 }
 
@@ -1118,18 +1143,27 @@ __global__ void gen_normal_kernel(float* out, long n, uint64_t seed) {
   const float u2 = (float)((h >> 16) & 0xFFFFFFull) * (1.0f / 16777216.0f);
   out[i] = sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
 }
-__global__ void gen_tokens_kernel(int64_t* out, long n, int vocab, uint64_t seed) {
+// sample b = [ids(S), attention_mask(stride - S)]: id j hashes stream index
+// b * S + j (the same ids as an unmasked plan); mask entries are 1
+__global__ void gen_tokens_kernel(int64_t* out, long n, int S, int stride, int vocab,
+                                  uint64_t seed) {
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const uint64_t h = splitmix64(seed * 0xD1B54A32D192ED03ull + (uint64_t)i);
+  const long b = i / stride, j = i - b * stride;
+  if (j >= S) {
+    out[i] = 1;
+    return;
+  }
+  const uint64_t h = splitmix64(seed * 0xD1B54A32D192ED03ull + (uint64_t)(b * S + j));
   out[i] = (int64_t)(((h >> 32) * (uint64_t)vocab) >> 32);
 }
 cudaError_t gen_normal(float* out, long n, uint64_t seed, cudaStream_t st) {
   gen_normal_kernel<<<nblk(n, 256), 256, 0, st>>>(out, n, seed);
   return cudaGetLastError();
 }
-cudaError_t gen_tokens(int64_t* out, long n, int vocab, uint64_t seed, cudaStream_t st) {
-  gen_tokens_kernel<<<nblk(n, 256), 256, 0, st>>>(out, n, vocab, seed);
+cudaError_t gen_tokens(int64_t* out, long n, int S, int stride, int vocab, uint64_t seed,
+                       cudaStream_t st) {
+  gen_tokens_kernel<<<nblk(n, 256), 256, 0, st>>>(out, n, S, stride, vocab, seed);
   return cudaGetLastError();
 }
 
@@ -1157,7 +1191,8 @@ cudaError_t flush_l2(void* buf, size_t bytes, cudaStream_t st) {
                                     int, float, cudaStream_t);                                 \
   template cudaError_t embed_ln<T>(const int32_t*, const T*, const T*, const T*, const float*, \
                                    const float*, T*, int, int, int, float, cudaStream_t);      \
-  template cudaError_t attention<T>(const T*, T*, int, int, int, int, cudaStream_t);           \
+  template cudaError_t attention<T>(const T*, T*, int, int, int, int, const uint32_t*,      \
+                                    cudaStream_t);           \
   template cudaError_t act_ew<T>(const T*, T*, long, int, cudaStream_t);                       \
   template cudaError_t output_gather<T>(const T*, float*, int, long, long, long, cudaStream_t); \
   template cudaError_t convert_f32<T>(const float*, T*, long, cudaStream_t);

@@ -119,7 +119,8 @@ cudaError_t tc_gemm_launch(const TcArgs& a, int bn, bool gather, const CUtensorM
                            const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& tr,
                            const CUtensorMap& ti, int num_sms, cudaStream_t st);
 
-cudaError_t attention_tc(const CUtensorMap& tm_qkv, bf16* out, int B, int H, cudaStream_t st);
+cudaError_t attention_tc(const CUtensorMap& tm_qkv, bf16* out, int B, int H,
+                         const uint32_t* keymask, cudaStream_t st);
 
 // ---- SIMT kernels (templated on storage type: float or bf16) -----------------
 struct GemmSimtArgs {
@@ -142,7 +143,8 @@ cudaError_t input_pack(const float* in, T* out, int B, int C, int H, int W, int 
                        cudaStream_t st);
 cudaError_t input_pack_s2d(const float* in, bf16* out, int B, int C, int H, int W, int shift,
                            int H2, int W2, cudaStream_t st);
-cudaError_t tokens_pack(const int64_t* in, int32_t* out, long n, int vocab, cudaStream_t st);
+cudaError_t tokens_pack(const int64_t* in, int32_t* out, uint32_t* mask, int B, int S,
+                        int stride, int vocab, cudaStream_t st);
 template <typename T>
 cudaError_t dwconv(const T* x, const T* w_rsc, const float* bias, T* y, int B, int H, int W,
                    int C, int R, int stride, int pad, int OH, int OW, int act, cudaStream_t st);
@@ -159,14 +161,16 @@ cudaError_t embed_ln(const int32_t* ids, const T* word, const T* pos, const T* t
                      const float* g, const float* b, T* y, int B, int S, int D, float eps,
                      cudaStream_t st);
 template <typename T>
-cudaError_t attention(const T* qkv, T* out, int B, int S, int H, int Dh, cudaStream_t st);
+cudaError_t attention(const T* qkv, T* out, int B, int S, int H, int Dh,
+                      const uint32_t* keymask, cudaStream_t st);
 template <typename T>
 cudaError_t act_ew(const T* x, T* y, long n, int act, cudaStream_t st);
 template <typename T>
 cudaError_t output_gather(const T* src, float* out, int B, long elems, long out_stride,
                           long offset, cudaStream_t st);
 cudaError_t gen_normal(float* out, long n, uint64_t seed, cudaStream_t st);
-cudaError_t gen_tokens(int64_t* out, long n, int vocab, uint64_t seed, cudaStream_t st);
+cudaError_t gen_tokens(int64_t* out, long n, int S, int stride, int vocab, uint64_t seed,
+                       cudaStream_t st);
 cudaError_t flush_l2(void* buf, size_t bytes, cudaStream_t st);
 
 template <typename T>

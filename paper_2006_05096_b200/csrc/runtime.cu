@@ -277,6 +277,7 @@ struct b2_plan {
   int input_kind = 0;
   long in_elems = 0, out_elems = 0;
   int vocab = 0;
+  int seq = 0;               // tokens per sample (TOKENS op)
   double flops = 0, weight_bytes = 0;
   std::vector<TensorRec> tensors;
   std::vector<Layer> layers;
@@ -762,13 +763,20 @@ int validate_ops(b2_plan* pl) {
     bool ok = true;
     switch (L.kind) {
       case OP_INPUT: ok = tok(p[0]) && p[1] > 0 && p[4] >= p[1]; break;
-      case OP_TOKENS: ok = tok(p[0]) && p[2] > 0; pl->vocab = p[2]; break;
+      case OP_TOKENS:
+        ok = tok(p[0]) && p[1] > 0 && p[2] > 0 && (!p[3] || tok(p[4])) &&
+             pl->in_elems == (long)p[1] * (p[3] ? 2 : 1);
+        pl->vocab = p[2];
+        pl->seq = p[1];
+        break;
       case OP_CONV: ok = tok(p[0]) && tok(p[1]) && (p[15] < 0 || tok(p[15])); break;
       case OP_LINEAR: ok = tok(p[0]) && tok(p[1]) && (p[8] < 0 || tok(p[8])); break;
       case OP_DWCONV: case OP_MAXPOOL: case OP_AVGPOOL: case OP_ACT: ok = tok(p[0]) && tok(p[1]); break;
       case OP_LAYERNORM: ok = tok(p[0]) && tok(p[1]) && (p[7] < 0 || tok(p[7])); break;
       case OP_EMBED: ok = tok(p[0]) && tok(p[1]); break;
-      case OP_ATTENTION: ok = tok(p[0]) && tok(p[1]) && p[3] == 64; break;
+      case OP_ATTENTION:
+        ok = tok(p[0]) && tok(p[1]) && p[3] == 64 && (!p[5] || tok(p[6]));
+        break;
       case OP_OUTPUT: {
         ok = p[0] >= 1 && p[0] <= 15;
         for (int j = 0; ok && j < p[0]; ++j)
@@ -806,7 +814,8 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
         break;
       case OP_TOKENS:
         CK(tokens_pack(static_cast<const int64_t*>(d_in), static_cast<int32_t*>(S.act[p[0]]),
-                       (long)B * p[1], p[2], st));
+                       p[3] ? static_cast<uint32_t*>(S.act[p[4]]) : nullptr, B, p[1],
+                       (int)pl->in_elems, p[2], st));
         ++launches;
         break;
       case OP_CONV:
@@ -995,10 +1004,13 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
         break;
       }
       case OP_ATTENTION:
+      {
+        const uint32_t* km = p[5] ? static_cast<const uint32_t*>(S.act[p[6]]) : nullptr;
         if (L.tc)
-          CK(attention_tc(S.tmA[li], reinterpret_cast<bf16*>(S.act[p[1]]), B, p[2], st));
+          CK(attention_tc(S.tmA[li], reinterpret_cast<bf16*>(S.act[p[1]]), B, p[2], km, st));
         else
-          CK(attention<T>(A(p[0]), A(p[1]), B, p[4], p[2], p[3], st));
+          CK(attention<T>(A(p[0]), A(p[1]), B, p[4], p[2], p[3], km, st));
+      }
         ++launches;
         break;
       case OP_ACT:
@@ -1476,7 +1488,8 @@ int graph_of(b2_plan* pl, BatchState& S, cudaGraphExec_t* out, bool second = fal
 int gen_inputs(b2_plan* pl, void* d_in, int batch, uint64_t seed, cudaStream_t st) {
   const long n = (long)batch * pl->in_elems;
   if (pl->input_kind == B2_IN_TOKENS_I64) {
-    CK(gen_tokens(static_cast<int64_t*>(d_in), n, pl->vocab, seed, st));
+    CK(gen_tokens(static_cast<int64_t*>(d_in), n, pl->seq, (int)pl->in_elems, pl->vocab, seed,
+                  st));
   } else {
     CK(gen_normal(static_cast<float*>(d_in), n, seed, st));
   }

@@ -56,9 +56,12 @@ _OP = struct.Struct("<I31i")
 # INPUT: fp32 sample laid out (C,H,W) -> NHWC activation with C zero-padded.
 OP_INPUT = 1
 P_IN_OUT, P_IN_C, P_IN_H, P_IN_W, P_IN_CPAD = range(5)
-# TOKENS: int64 ids [seq] -> int32 ids tensor
+# TOKENS: int64 ids [seq] -> int32 ids tensor.  With has_mask the sample is
+# [ids(seq), attention_mask(seq)] (int64, 1 = attend, 0 = padding) and the
+# mask is packed into a key-validity bit tensor: (seq + 31) // 32 int32 words
+# per sample, bit j % 32 of word j // 32 = key j valid.
 OP_TOKENS = 2
-P_TK_OUT, P_TK_SEQ, P_TK_VOCAB = range(3)
+P_TK_OUT, P_TK_SEQ, P_TK_VOCAB, P_TK_HASMASK, P_TK_MASK = range(5)
 # CONV: out = act(conv(in, w) + bias + res); w [Cout, R, S, Cin] (OHWI)
 OP_CONV = 3
 (P_CV_IN, P_CV_OUT, P_CV_W, P_CV_B, P_CV_H, P_CV_W_, P_CV_CIN, P_CV_COUT, P_CV_R, P_CV_S,
@@ -87,9 +90,12 @@ OP_LAYERNORM = 8
 OP_EMBED = 9
 (P_EM_IDS, P_EM_OUT, P_EM_WORD, P_EM_POS, P_EM_TYPE, P_EM_G, P_EM_B, P_EM_D, P_EM_SEQ,
  P_EM_VOCAB, P_EM_EPS) = range(11)
-# ATTENTION: qkv [seq, 3*H*Dh] (Q|K|V, head-major) -> out [seq, H*Dh]; no mask
+# ATTENTION: qkv [seq, 3*H*Dh] (Q|K|V, head-major) -> out [seq, H*Dh];
+# softmax(QK^T / sqrt(Dh) + bias) V with bias = 0 for valid keys and
+# float32 min for padded keys (transformers' extended attention mask) when
+# has_mask (the mask tensor is TOKENS' packed key bits)
 OP_ATTENTION = 10
-P_AT_QKV, P_AT_OUT, P_AT_HEADS, P_AT_DH, P_AT_SEQ = range(5)
+P_AT_QKV, P_AT_OUT, P_AT_HEADS, P_AT_DH, P_AT_SEQ, P_AT_HASMASK, P_AT_MASK = range(7)
 # OUTPUT: concat per sample into the fp32 output: p0 = n, then (tensor, offset)
 OP_OUTPUT = 11
 # ACT: standalone activation over elems per sample

@@ -534,3 +534,24 @@ class CellRunner:
             self._inst.clear()
         for i in insts:
             self.profiler.teardown(i)
+
+
+def nvml_hooks(provider, runner: CellRunner, pid_of: Callable[[str], Optional[int]]):
+    """``sample`` and ``ours_only`` for ControllerSweep on real GPUs: device
+    utilisation from NVML, and "every compute process on this GPU is one of
+    our workers (or this process)" from NVML's process list."""
+    import os
+
+    def sample() -> dict:
+        return provider.sample()
+
+    def ours_only(dev: str) -> bool:
+        idx = int(dev.split(":")[1])
+        mine = {os.getpid()}
+        for inst in runner.instances_on(dev):
+            pid = pid_of(inst.id)
+            if pid is not None:
+                mine.add(pid)
+        return provider.compute_pids(idx) <= mine
+
+    return sample, ours_only

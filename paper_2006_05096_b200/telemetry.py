@@ -148,6 +148,15 @@ class NvmlProvider(DeviceProvider):
             raise ProviderFailure(f"NVML sampling failed: {exc}") from exc
         return out
 
+    def compute_pids(self, index: int) -> set:
+        """Pids holding a compute context on GPU `index` (NVML shares the
+        host PID namespace here: tools/nvml_probe.py saw the load's own pid)."""
+        try:
+            return {p.pid for p in self._nv.nvmlDeviceGetComputeRunningProcesses(
+                self._handles[index])}
+        except self._nv.NVMLError as exc:
+            raise ProviderFailure(f"NVML process list failed: {exc}") from exc
+
     def process_stats(self, index: int, pid: int) -> tuple[float, int]:
         """(SM share in [0,1], used GPU memory bytes) of `pid` on GPU `index`."""
         h = self._handles[index]

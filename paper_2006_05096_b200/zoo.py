@@ -295,14 +295,17 @@ def emit_vgg(model, name="vgg16") -> P.PlanBuilder:
 # -- BERT ---------------------------------------------------------------------------
 
 
-def emit_bert(model, seq: int = 128, name="bert") -> P.PlanBuilder:
+def emit_bert(model, seq: int = 128, name="bert", mask: bool = True) -> P.PlanBuilder:
+    """BertModel -> plan.  ``mask``: the sample is [input_ids, attention_mask]
+    (padded batches, transformers semantics); the profiling payload sets the
+    mask to ones (attention_mask=1)."""
     cfg = model.config
     D, H = cfg.hidden_size, cfg.num_attention_heads
     Dh = D // H
     eps = cfg.layer_norm_eps
     b = P.PlanBuilder(name)
     b.input_kind = P.IN_TOKENS
-    b.in_elems = seq
+    b.in_elems = 2 * seq if mask else seq
     flops = 0
 
     def lin(x, module, rows, act=P.ACT_NONE, res=-1, weight=None, bias=None, astride=None):
@@ -324,7 +327,8 @@ def emit_bert(model, seq: int = 128, name="bert") -> P.PlanBuilder:
         return y
 
     ids = b.tensor(seq, kind=P.T_IDS)
-    b.op_p(P.OP_TOKENS, [ids, seq, cfg.vocab_size])
+    mbits = b.tensor((seq + 31) // 32, kind=P.T_IDS) if mask else 0
+    b.op_p(P.OP_TOKENS, [ids, seq, cfg.vocab_size, int(mask), mbits])
     emb = model.embeddings
     x = b.tensor(seq, D)
     b.op_p(P.OP_EMBED, [ids, x, b.weight(emb.word_embeddings.weight.detach().numpy()),
@@ -341,7 +345,7 @@ def emit_bert(model, seq: int = 128, name="bert") -> P.PlanBuilder:
                                for m in (sa.query, sa.key, sa.value)], 0)
         qkv = lin(x, None, seq, weight=wqkv, bias=bqkv)
         ctx = b.tensor(seq, D)
-        b.op_p(P.OP_ATTENTION, [qkv, ctx, H, Dh, seq])
+        b.op_p(P.OP_ATTENTION, [qkv, ctx, H, Dh, seq, int(mask), mbits])
         flops += 4 * H * seq * seq * Dh
         ao = layer.attention.output
         a = lin(ctx, ao.dense, seq, res=x)
@@ -354,6 +358,7 @@ def emit_bert(model, seq: int = 128, name="bert") -> P.PlanBuilder:
     b.op_p(P.OP_OUTPUT, [2, x, 0, pooled, seq * D])
     b.meta["flops_per_sample"] = flops
     b.meta["seq"] = seq
+    b.meta["attention_mask"] = bool(mask)
     return b
 
 

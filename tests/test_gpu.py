@@ -130,7 +130,10 @@ def test_gen_input_matches_restatement(gpu_required):
             buf = torch.empty(n, dtype=torch.int64, device="cuda")
             plan.gen_input(buf.data_ptr(), 3, 99)
             torch.cuda.synchronize()
-            assert np.array_equal(buf.cpu().numpy(), gen_ref.tokens(n, 30522, 99))
+            pl = P.decode(blob)
+            tk = next(o for o in pl.ops if o.kind == P.OP_TOKENS)
+            want = gen_ref.plan_tokens(3, tk[P.P_TK_SEQ], 30522, 99, bool(tk[P.P_TK_HASMASK]))
+            assert np.array_equal(buf.cpu().numpy(), want)
         else:
             buf = torch.empty(n, dtype=torch.float32, device="cuda")
             plan.gen_input(buf.data_ptr(), 3, 99)

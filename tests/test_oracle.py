@@ -55,7 +55,8 @@ def test_oracle_matches_framework_forward(name):
     md = model.double()
     with torch.no_grad():
         if name == "bert":
-            r = md(input_ids=torch.from_numpy(x))
+            r = md(input_ids=torch.from_numpy(x[:, :128]),
+                   attention_mask=torch.from_numpy(x[:, 128:]))
             ref = torch.cat([r.last_hidden_state.reshape(1, -1), r.pooler_output], 1).numpy()
         else:
             ref = md(torch.from_numpy(x.astype(np.float64)).reshape(1, 3, 224, 224)).numpy()
@@ -63,6 +64,47 @@ def test_oracle_matches_framework_forward(name):
     assert plan_ref.normwise_err(out, ref) < 2e-5
     assert pl.meta["flops_per_sample"] == {"resnet50": 8178368512, "mobilenet_v2": 601548544,
                                            "vgg16": VGG16_FLOPS, "bert": 22348431360}[name]
+
+
+def padded_bert_inputs(pl, lengths, seed=7):
+    """Token ids + attention_mask for a padded batch: sample i attends to its
+    first lengths[i] tokens (the rest are [PAD] = 0, as a tokenizer pads)."""
+    S = 128
+    x = plan_ref.make_inputs(pl, len(lengths), seed)
+    for i, n in enumerate(lengths):
+        x[i, n:S] = 0
+        x[i, S:] = 0
+        x[i, S:S + n] = 1
+    return x
+
+
+def test_oracle_bert_padded_batch_matches_transformers():
+    """QK^T -> mask -> softmax -> PV: a padded batch (lengths 128, 77, 5)
+    through the oracle equals transformers' BertModel with attention_mask,
+    padded query rows included."""
+    import torch
+    torch.set_num_threads(8)
+    model = zoo.make_torch_model("bert", 0)
+    pl = P.decode(zoo.emit_torch("bert", model).build(P.DT_FP32))
+    x = padded_bert_inputs(pl, [128, 77, 5])
+    out = plan_ref.forward(pl, x)
+    with torch.no_grad():
+        r = model.double()(input_ids=torch.from_numpy(x[:, :128]),
+                           attention_mask=torch.from_numpy(x[:, 128:]))
+    ref = torch.cat([r.last_hidden_state.reshape(3, -1), r.pooler_output], 1).numpy()
+    assert plan_ref.normwise_err(out, ref) < 2e-5
+    # the mask matters: without it the short samples change completely
+    nomask = x.copy()
+    nomask[:, 128:] = 1
+    assert plan_ref.normwise_err(plan_ref.forward(pl, nomask)[2], ref[2]) > 0.1
+
+
+def test_keymask_pack_roundtrip():
+    rng = np.random.default_rng(0)
+    m = rng.random((5, 128)) < 0.5
+    w = plan_ref.pack_keymask(m)
+    assert w.shape == (5, 4) and np.array_equal(plan_ref.unpack_keymask(w, 128), m)
+    assert plan_ref.pack_keymask(np.ones((1, 128), bool)).tolist() == [[-1, -1, -1, -1]]
 
 
 def test_bf16_emulation_is_round_to_nearest_even():
