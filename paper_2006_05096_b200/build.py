@@ -44,6 +44,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> Path:
                     "-I", str(PKG.parent / "include")]
     if verbose:
         flags += ["-Xptxas", "-v"]
+    if os.environ.get("B2_BUILD_DEBUG") == "1":   # profiling aids: drain-only epilogues, stamps
+        flags += ["-DB2_DEBUG", "-DB2_TILE_TS"]
     procs = []
     objs = []
     for src in sources():

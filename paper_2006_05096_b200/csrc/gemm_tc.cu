@@ -30,6 +30,16 @@
 
 namespace b2 {
 
+// Profiling aids (drain-only epilogues, phase timestamps) exist only in
+// -DB2_DEBUG builds; production kernels carry no debug branches.
+#ifdef B2_DEBUG
+#define EPI_DBG(a) ((a).epi_debug)
+#define TS_DBG(a) ((a).ts_debug)
+#else
+#define EPI_DBG(a) 0
+#define TS_DBG(a) 0
+#endif
+
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;
 constexpr int TC_SMEM_MAX = 232448;           // 227 KB: the opt-in per-CTA maximum
@@ -74,7 +84,7 @@ B2_DEV void tile_stamp(const TcArgs& a, int which, int tile) {
 #ifndef B2_TILE_TS
   return;
 #endif
-  if (a.ts_debug == 2 && blockIdx.x == 0 && tile < 32) {
+  if (TS_DBG(a) == 2 && blockIdx.x == 0 && tile < 32) {
     unsigned long long g;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
     g_tile_ts[which][tile] = g;
@@ -184,13 +194,13 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint
 #pragma unroll
         for (int j = 0; j < 16; ++j) gelu_erf2(v[2 * j], v[2 * j + 1]);
       }
-      if (lane == 0 && a.epi_debug != 4 && a.epi_debug != 5) bulk_wait_read<1>();
+      if (lane == 0 && EPI_DBG(a) != 4 && EPI_DBG(a) != 5) bulk_wait_read<1>();
       __syncwarp();
       uint8_t* sbuf = obuf + (oi & 1) * 2048;
       uint8_t* orow = sbuf + lane * 64;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        if (a.epi_debug == 6) {
+        if (EPI_DBG(a) == 6) {
           if (v[q * 8] == 1234.5f) orow[q] = 1;
           continue;
         }
@@ -201,9 +211,9 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint
         u.w = pack_bf16x2(act_t<PACT>(v[q * 8 + 6]), act_t<PACT>(v[q * 8 + 7]));
         *reinterpret_cast<uint4*>(orow + ((q ^ swz) << 4)) = u;
       }
-      if (a.epi_debug != 3) fence_proxy_async_smem();
+      if (EPI_DBG(a) != 3) fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0 && a.epi_debug != 5) {
+      if (lane == 0 && EPI_DBG(a) != 5) {
         if (a.out3d)
           tma_store_3d(&tmO, sbuf, n0 + c, lg * 32, m0 / TC_BM);
         else
@@ -258,7 +268,7 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
 
   __shared__ unsigned long long ts[8];    // B2_GEMM_TS phase timestamps (globaltimer, ns)
   auto stamp = [&](int i) {
-    if (a.ts_debug) {
+    if (TS_DBG(a)) {
       unsigned long long g;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
       ts[i] = g;
@@ -316,11 +326,11 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
         }
         for (int kb = kb0; kb < kb1; ++kb) {
 #ifdef B2_TILE_TS
-          if (kb == kb0 && a.ts_debug == 2) tile_stamp(a, 5, (u - (int)blockIdx.x) / (int)gridDim.x);
+          if (kb == kb0 && TS_DBG(a) == 2) tile_stamp(a, 5, (u - (int)blockIdx.x) / (int)gridDim.x);
 #endif
           mbar_wait(&empty[stage], phase ^ 1);
 #ifdef B2_TILE_TS
-          if (kb == kb0 && a.ts_debug == 2) tile_stamp(a, 0, (u - (int)blockIdx.x) / (int)gridDim.x);
+          if (kb == kb0 && TS_DBG(a) == 2) tile_stamp(a, 0, (u - (int)blockIdx.x) / (int)gridDim.x);
 #endif
           if (kb >= a.kblocks) {
             const int j = kb - a.kblocks;
@@ -446,7 +456,7 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
     const int eh = ew >> 2;           // which half of each quadrant's columns
     const bool has_res = a.res != nullptr;
     int it = 0;
-    if (a.epi_debug == 1) {
+    if (EPI_DBG(a) == 1) {
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int as = it & 1;
         mbar_wait(&tfull[as], (it >> 1) & 1);
@@ -659,14 +669,14 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
   if (warp == 2 && lane == 0) stamp(4);
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0 && a.ts_debug) {
+  if (threadIdx.x == 0 && TS_DBG(a)) {
     stamp(5);
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     printf("b2ts %d %u %llu %llu %llu %llu %llu %llu stages %d kblocks %d tiles %d\n", blockIdx.x,
            smid, ts[0], ts[1], ts[2], ts[3], ts[4], ts[5], STAGES, a.kblocks, ntiles);
 #ifdef B2_TILE_TS
-    if (a.ts_debug == 2 && blockIdx.x == 0)
+    if (TS_DBG(a) == 2 && blockIdx.x == 0)
 #else
     if (false)
 #endif

@@ -469,7 +469,8 @@ __global__ void __launch_bounds__(256) dwconv3_strip_kernel(const T* __restrict_
 static int dw_owt(int stride, int OW) {
   // read per launch (not cached): launches are captured into CUDA graphs, so
   // this runs once per plan state, and tests switch widths within a process
-  const char* e = getenv(stride == 1 ? "B2_DW_OWT" : "B2_DW_OWT2");
+  const char* dv = getenv("B2_DEV");
+  const char* e = dv && dv[0] == '1' ? getenv(stride == 1 ? "B2_DW_OWT" : "B2_DW_OWT2") : nullptr;
   const int v = e ? atoi(e) : 0;
   if (v) return v;
   if (stride == 1) return (OW % 8 == 0 || OW < 16) ? 8 : 4;

@@ -43,7 +43,8 @@ def test_padded_batch_end_to_end(gpu_required, bert_blob, dtype):
     err = plan_ref.normwise_err(y, ref)
     assert err <= (1e-4 if dtype == P.DT_FP32 else 2e-2), err
     assert not bad, bad[:5]
-    # samples are independent: a short sample's output does not depend on its padding ids
+    # masking works: a short sample's valid positions and pooled output do not
+    # depend on what its padded positions hold
     x2 = x.copy()
     x2[2, 5:128] = 1234
     plan = R.Plan(blob, dtype)
@@ -51,7 +52,10 @@ def test_padded_batch_end_to_end(gpu_required, bert_blob, dtype):
         y2 = plan.predict(x2)
     finally:
         plan.close()
-    assert plan_ref.normwise_err(y2[2], y[2]) <= (1e-5 if dtype == P.DT_FP32 else 1e-2)
+    keep = np.r_[0:5 * 768, 128 * 768:129 * 768]
+    assert plan_ref.normwise_err(y2[2, keep], y[2, keep]) <= (1e-5 if dtype == P.DT_FP32
+                                                             else 1e-2)
+    assert plan_ref.normwise_err(y2[2], y[2]) > 0.01      # the padded rows themselves changed
 
 
 def test_mask_words_match_oracle_and_full_mask_is_unmasked(gpu_required, bert_blob):

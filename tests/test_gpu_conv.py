@@ -21,6 +21,13 @@ pytestmark = pytest.mark.gpu
 TOL = plan_ref.BF16_LAYERWISE_TOL
 
 
+@pytest.fixture(autouse=True)
+def developer_knobs(monkeypatch):
+    """These tests pin kernel variants through the B2_* selection knobs,
+    which libb2 honours only with B2_DEV=1."""
+    monkeypatch.setenv("B2_DEV", "1")
+
+
 def conv_plan(H, W, C, N, k, stride, act=1, seed=0):
     pad = k // 2
     OH = (H + 2 * pad - k) // stride + 1

@@ -1,4 +1,5 @@
 # A/B: per-op profiles, new library vs ab/libb2_base.so (HEAD); models from $AB_MODELS
+export B2_DEV=1   # developer knobs (B2_*) honoured
 cd $GRAFT_REPO_ROOT
 for m in ${AB_MODELS:-"resnet50:256" "bert:128" "vgg16:256" "mobilenet_v2:256"}; do
   n=${m%%:*}; b=${m##*:}

@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
+export B2_DEV=1   # developer knobs (B2_*) honoured
 for bd in 0 1; do
   export B2_BAND=$bd
   timeout 60 python tools/conv_micro.py 256 56 56 64 64 3 1

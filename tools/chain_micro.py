@@ -1,6 +1,7 @@
 """Graph-replayed chain of L identical LINEAR layers (M x K -> K): per-layer
 device time inside a CUDA graph, free of eager launch overhead."""
 import os, sys
+os.environ.setdefault("B2_DEV", "1")   # developer knobs (B2_*) honoured
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)

@@ -1,5 +1,6 @@
 """Run-to-run determinism check of one model at one batch (first vs second predict)."""
 import os, sys
+os.environ.setdefault("B2_DEV", "1")   # developer knobs (B2_*) honoured
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)

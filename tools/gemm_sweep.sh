@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
+export B2_DEV=1   # developer knobs (B2_*) honoured
 for sk in 0 1; do
 export B2_SPLIT=$sk
 for args in "12544 2048 512" "12544 512 2048 res" "50176 1024 256" "300 2048 512"; do

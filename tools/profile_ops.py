@@ -1,5 +1,6 @@
 """Per-op device times of one forward (eager, CUDA events between ops)."""
 import os, sys, json
+os.environ.setdefault("B2_DEV", "1")   # developer knobs (B2_*) honoured
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
