@@ -11,7 +11,11 @@ overlap the forward on separate streams, as a serving pipeline would).
 
 Multi-GPU (torchrun): one process per GPU, each runs its own replica of the
 step (the sweep shards by cell with no data-path collective: "scaling": weak);
-a barrier + max-over-ranks brackets the timed region.
+a barrier + max-over-ranks brackets the timed region.  ``sweep_c4`` is the
+north star's multi-GPU quantity: the C4 profile sweep (5 models x 9 batch
+sizes) partitioned over the ranks (request-sharded heavy cells, setup-aware
+LPT, no collective but the final gather of sample documents), wall time max
+over ranks.
 
 ``--impl reference`` times the CPU implementation of the path (the numpy
 oracle port of the forward, oracle/plan_ref.py, on all host cores) on a
@@ -197,6 +201,69 @@ def per_op_table(plan, blob: bytes, batch: int, ms_per_step: float, pk: dict,
     return rows[:top]
 
 
+C4_MODELS = ("mlp", "mobilenet_v2", "resnet50", "bert", "vgg16")
+C4_BATCHES = (1, 2, 4, 8, 16, 32, 64, 128, 256)
+# algorithmic FLOPs per sample (the plans' own flops_per_sample)
+C4_FLOPS = {"mlp": 406528, "mobilenet_v2": 601548544, "resnet50": 8178368512,
+            "bert": 22348431360, "vgg16": 30940528640}
+
+
+def sweep_leg(rank: int, world: int, barrier, max_over_ranks, requests: int = 100,
+              warmup: int = 10) -> dict:
+    """The C4 profile sweep (BASELINE configs[3]: 5 models x 9 batch sizes,
+    n=100 requests + 10 warm-up per cell, device-timed) over the ranks of
+    this job, one process per GPU and no data-path collective: heavy cells
+    request-sharded, units partitioned by the setup-aware LPT
+    (sweeprun.partitioned_sweep), each rank loading only the models of its
+    share and measuring its units with b2_bench; only the samples documents
+    are gathered.  Wall time = barrier to barrier, max over ranks, plan
+    loading (the per-GPU worker start) included."""
+    import numpy as np
+    from paper_2006_05096_b200 import plan as P, runtime as R
+    from paper_2006_05096_b200.profiler.stats import LatencySamples
+    from paper_2006_05096_b200.profiler.types import ProfilingJob, SweepSpec
+    from paper_2006_05096_b200.sweeprun import cell_cost, partitioned_sweep
+    jobs = [ProfilingJob(f"c4-{m}", m, m, SweepSpec(batch_sizes=list(C4_BATCHES),
+                                                    devices=["gpu:*"], backends=["b200"],
+                                                    protocols=["grpc-style"],
+                                                    requests_per_cell=requests,
+                                                    warmup_requests=warmup)) for m in C4_MODELS]
+    cost = lambda j, c: cell_cost(C4_FLOPS[j.variant_id], c, c.shard_requests(requests), warmup)
+    plans, busy = {}, [0.0]
+
+    def measure(job, unit):
+        m = job.variant_id
+        if m not in plans:
+            plans[m] = R.Plan(build_plan(m, P.DT_BF16), P.DT_BF16)
+        lat, comp = plans[m].bench(unit.batch_size, unit.shard_requests(requests), warmup,
+                                   seed=unit.shard)
+        busy[0] += float(comp[-1]) / 1e3
+        return LatencySamples([float(v) for v in lat], [float(v) for v in comp])
+
+    barrier()
+    t0 = time.perf_counter()
+    results = partitioned_sweep(jobs, rank, world, measure, cost, setup_s=lambda j: 1.0)
+    barrier()
+    wall = max_over_ranks(time.perf_counter() - t0)
+    dev = max_over_ranks(busy[0])
+    for pl in plans.values():
+        pl.close()
+    out = {"wall_s": round(wall, 3), "gpus": world, "cells": len(results) if rank == 0 else None,
+           "busiest_rank_device_s": round(dev, 3),
+           "config": "C4: " + ",".join(C4_MODELS) + " x batches 1..256, n=100 + 10 warm-up "
+                     "per cell, bf16, request-sharded heavy cells, setup-aware LPT over ranks",
+           "timing": "host wall clock, barrier to barrier, max over ranks (plan builds = "
+                     "worker starts included)"}
+    if rank == 0:
+        out["sharded_cells"] = sorted(f"{r.variant_id}:{r.batch_size}"
+                                      for r in results if "," in r.device)
+        out["per_cell"] = {f"{r.variant_id}:{r.batch_size}": [round(r.peak_throughput, 1),
+                                                              round(r.p50_latency_ms, 4),
+                                                              round(r.p99_latency_ms, 4)]
+                           for r in results}
+    return out
+
+
 def run_ours(args) -> dict | None:
     rank, local, world = dist_env()
     if world > 1:
@@ -242,6 +309,9 @@ def run_ours(args) -> dict | None:
     barrier()
     e2e_ms = max_over_ranks(float(ecomp[-1]))
     e2e_value = world * K * B / (e2e_ms / 1e3)
+    sweep = None
+    if not args.no_c4:
+        sweep = sweep_leg(rank, world, barrier, max_over_ranks)
     if rank != 0:
         if pg is not None:
             pg.destroy_process_group()
@@ -271,6 +341,8 @@ def run_ours(args) -> dict | None:
         "gpu_launches": int(K * plan.launches_per_forward),
         "clocks": clk.summary(),
     }
+    if sweep is not None:
+        line["sweep_c4"] = sweep
     line["roofline"] = roofline(plan, args.model, B, elapsed_ms / K, pk)
     line["roofline"]["per_op"] = per_op_table(plan, blob, B, elapsed_ms / K, pk)
     if not args.no_sweep:
@@ -334,6 +406,8 @@ def main() -> int:
     ap.add_argument("--dtype", choices=["bf16", "fp32"], default="bf16")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c4", action="store_true",
+                    help="skip the C4 profile-sweep wall-time leg (all ranks)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     line = run_reference(args) if args.impl == "reference" else run_ours(args)
