@@ -113,37 +113,45 @@ __global__ void __launch_bounds__(CH_THREADS, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    // whole warp converged, one elected lane issues (warp-uniform operands, no
+    // per-TMA ELECT/R2UR waterfall; see gemm_tc.cu's producers)
+    {
       int st = 0, s2 = 0;
       uint32_t ph = 0, ph2 = 0;
-      auto load_g1 = [&](int m0, int c) {
+      const int kblocks = a.kblocks, fold = a.fold_kind;
+      const uint32_t full_lo = uniform_u32(smem_u32(&full[0]));
+      const uint32_t empty_lo = uniform_u32(smem_u32(&empty[0]));
+      const uint32_t b2full_lo = uniform_u32(smem_u32(&b2full[0]));
+      const uint32_t b2empty_lo = uniform_u32(smem_u32(&b2empty[0]));
+      const uint32_t ring_lo = uniform_u32(smem_u32(sRing));
+      const uint32_t sB2_lo = uniform_u32(smem_u32(sB2));
+      auto load_g1 = [&](int m0, int c, int fw, int fh, int fim) {
         const int n0 = c * CH_BN;
         for (int kb = 0; kb < KT1; ++kb) {
-          mbar_wait(&empty[st], ph ^ 1);
-          uint8_t* dA = sRing + st * CH_STAGE;
-          uint8_t* dB = dA + CH_A_BYTES;
-          mbar_arrive_expect_tx(&full[st], CH_STAGE);
-          if (kb < a.kblocks) {
-            tma_load_2d(dA, &tmA, &full[st], kb * CH_BK, m0);
-            tma_load_2d(dB, &tmB1, &full[st], kb * CH_BK, n0);
-          } else {
-            const int j = kb - a.kblocks;
-            if (a.fold_kind == 0) {           // residual x identity
-              tma_load_2d(dA, &tmR, &full[st], n0 + j * CH_BK, m0);
-              tma_load_2d(dB, &tmI, &full[st], j * CH_BK, 0);
-            } else {                          // projection shortcut x Wd
-              if (a.fold_kind == 1) {
-                tma_load_2d(dA, &tmR, &full[st], j * CH_BK, m0);
-              } else {
-                const int im = m0 / a.OHW;
-                const int rem = m0 - im * a.OHW;
-                const int oh = rem / a.OW;
-                tma_load_im2col_4d(dA, &tmR, &full[st], j * CH_BK, (rem - oh * a.OW) * a.stride,
-                                   oh * a.stride, im, 0, 0);
+          mbar_wait_u32(empty_lo + st * 8, ph ^ 1);
+          const uint32_t dA = ring_lo + st * CH_STAGE;
+          const uint32_t dB = dA + CH_A_BYTES;
+          const uint32_t fb = full_lo + st * 8;
+          if (elect_one()) {
+            mbar_arrive_expect_tx_u32(fb, CH_STAGE);
+            if (kb < kblocks) {
+              tma_load_2d_u32(dA, &tmA, fb, kb * CH_BK, m0);
+              tma_load_2d_u32(dB, &tmB1, fb, kb * CH_BK, n0);
+            } else {
+              const int j = kb - kblocks;
+              if (fold == 0) {                  // residual x identity
+                tma_load_2d_u32(dA, &tmR, fb, n0 + j * CH_BK, m0);
+                tma_load_2d_u32(dB, &tmI, fb, j * CH_BK, 0);
+              } else {                          // projection shortcut x Wd
+                if (fold == 1)
+                  tma_load_2d_u32(dA, &tmR, fb, j * CH_BK, m0);
+                else
+                  tma_load_im2col_4d_u32(dA, &tmR, fb, j * CH_BK, fw, fh, fim, 0, 0);
+                tma_load_2d_u32(dB, &tmI, fb, j * CH_BK, n0);
               }
-              tma_load_2d(dB, &tmI, &full[st], j * CH_BK, n0);
             }
           }
+          __syncwarp();
           if (++st == ST) {
             st = 0;
             ph ^= 1;
@@ -152,9 +160,13 @@ __global__ void __launch_bounds__(CH_THREADS, 1)
       };
       auto load_g2 = [&](int c) {
         for (int kb = 0; kb < KT2; ++kb) {
-          mbar_wait(&b2empty[s2], ph2 ^ 1);
-          mbar_arrive_expect_tx(&b2full[s2], (uint32_t)B2_BYTES);
-          tma_load_2d(sB2 + s2 * B2_BYTES, &tmB2, &b2full[s2], c * CH_BN + kb * CH_BK, 0);
+          mbar_wait_u32(b2empty_lo + s2 * 8, ph2 ^ 1);
+          if (elect_one()) {
+            mbar_arrive_expect_tx_u32(b2full_lo + s2 * 8, (uint32_t)B2_BYTES);
+            tma_load_2d_u32(sB2_lo + s2 * B2_BYTES, &tmB2, b2full_lo + s2 * 8,
+                            c * CH_BN + kb * CH_BK, 0);
+          }
+          __syncwarp();
           if (++s2 == S2) {
             s2 = 0;
             ph2 ^= 1;
@@ -163,9 +175,17 @@ __global__ void __launch_bounds__(CH_THREADS, 1)
       };
       for (int t = blockIdx.x; t < a.tiles_m; t += gridDim.x) {
         const int m0 = chain_mtile(a, t) * CH_BM;
-        load_g1(m0, 0);
+        int fw = 0, fh = 0, fim = 0;     // strided shortcut: its input pixel of row m0
+        if (fold == 2) {
+          fim = m0 / a.OHW;
+          const int rem = m0 - fim * a.OHW;
+          const int oh = rem / a.OW;
+          fw = (rem - oh * a.OW) * a.stride;
+          fh = oh * a.stride;
+        }
+        load_g1(m0, 0, fw, fh, fim);
         for (int c = 1; c < C; ++c) {
-          load_g1(m0, c);
+          load_g1(m0, c, fw, fh, fim);
           load_g2(c - 1);
         }
         load_g2(C - 1);

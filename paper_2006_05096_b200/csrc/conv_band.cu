@@ -155,10 +155,21 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    // whole warp converged, one elected lane issues (see gemm_tc.cu)
+    {
+      const uint32_t afull_lo = uniform_u32(smem_u32(&afull[0]));
+      const uint32_t aempty_lo = uniform_u32(smem_u32(&aempty[0]));
+      const uint32_t bfull_lo = uniform_u32(smem_u32(&bfull[0]));
+      const uint32_t bempty_lo = uniform_u32(smem_u32(&bempty[0]));
+      const uint32_t sA_lo = uniform_u32(smem_u32(sA)), sB_lo = uniform_u32(smem_u32(sB));
+      const uint32_t a_box = a.a_box_bytes, a_stage = a.a_stage_bytes;
       if constexpr (BRES) {
-        mbar_arrive_expect_tx(bres, (uint32_t)(a.kblocks * B_BLOCK));
-        for (int kb = 0; kb < a.kblocks; ++kb) tma_load_2d(sB + kb * B_BLOCK, &tmB, bres, kb * 64, 0);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(bres, (uint32_t)(a.kblocks * B_BLOCK));
+          for (int kb = 0; kb < a.kblocks; ++kb)
+            tma_load_2d(sB + kb * B_BLOCK, &tmB, bres, kb * 64, 0);
+        }
+        __syncwarp();
       }
       int as = 0, bs = 0;
       uint32_t aph = 0, bph = 0;
@@ -170,11 +181,14 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
         const int seg = rest % a.nseg;
         const int band = (rest / a.nseg) % a.nbands;
         const int img = rest / a.nseg / a.nbands;
+        const int ax = seg * a.seg_w + a.x0, ay = band * a.bh + a.y0;
         for (int cg = 0; cg < a.CG; ++cg) {
-          mbar_wait(&aempty[as], aph ^ 1);
-          mbar_arrive_expect_tx(&afull[as], (uint32_t)a.a_box_bytes);
-          tma_load_4d(sA + as * a.a_stage_bytes, &tmA, &afull[as], cg * CGW,
-                      seg * a.seg_w + a.x0, band * a.bh + a.y0, img);
+          mbar_wait_u32(aempty_lo + as * 8, aph ^ 1);
+          if (elect_one()) {
+            mbar_arrive_expect_tx_u32(afull_lo + as * 8, a_box);
+            tma_load_4d_u32(sA_lo + as * a_stage, &tmA, afull_lo + as * 8, cg * CGW, ax, ay, img);
+          }
+          __syncwarp();
           if (++as == a.a_stages) {
             as = 0;
             aph ^= 1;
@@ -183,9 +197,13 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
             // one 64-wide K block per (tap, group): K index tap * C + cg * 64
 #pragma unroll 1
             for (int t = 0; t < TAPS; ++t) {
-              mbar_wait(&bempty[bs], bph ^ 1);
-              mbar_arrive_expect_tx(&bfull[bs], (uint32_t)B_BLOCK);
-              tma_load_2d(sB + bs * B_BLOCK, &tmB, &bfull[bs], (t * a.CG + cg) * 64, nt * BN);
+              mbar_wait_u32(bempty_lo + bs * 8, bph ^ 1);
+              if (elect_one()) {
+                mbar_arrive_expect_tx_u32(bfull_lo + bs * 8, (uint32_t)B_BLOCK);
+                tma_load_2d_u32(sB_lo + bs * B_BLOCK, &tmB, bfull_lo + bs * 8,
+                                (t * a.CG + cg) * 64, nt * BN);
+              }
+              __syncwarp();
               if (++bs == a.b_stages) {
                 bs = 0;
                 bph ^= 1;

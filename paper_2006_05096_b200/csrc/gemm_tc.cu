@@ -306,96 +306,119 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      const int cpb = a.C >> 6;   // im2col: 64-channel K blocks per filter tap
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const int t = u % ntiles;
-        int kb0, kb1;
-        split_range(u / ntiles, a.nsplit, KT, kb0, kb1);
-        const int m0 = mtile_of(a, t) * TC_BM;
-        const int n0 = (t % a.tiles_n) * BN;
-        int iw0 = 0, ih0 = 0, img = 0;
-        if (!GATHER && a.a_im2col) {
-          img = m0 / a.OHW;
-          const int rem = m0 - img * a.OHW;
-          const int oh = rem / a.OW;
-          ih0 = oh * a.stride - a.pad;
-          iw0 = (rem - oh * a.OW) * a.stride - a.pad;
-        }
-        for (int kb = kb0; kb < kb1; ++kb) {
+    // Whole warp converged, one elected lane issues (see the CTA-pair kernel:
+    // warp-uniform operands, no per-TMA waterfall, no divisions per K block).
+    const int Cin = a.C;
+    const int Stap = a.S;
+    const int kblocks = a.kblocks;
+    const int im2col = a.a_im2col;
+    const int fold = a.fold_kind;
+    const uint32_t full_lo = uniform_u32(smem_u32(&full[0]));
+    const uint32_t empty_lo = uniform_u32(smem_u32(&empty[0]));
+    const uint32_t sA_lo = uniform_u32(smem_u32(sA)), sB_lo = uniform_u32(smem_u32(sB));
+    const uint32_t a_bytes = GATHER ? 0u : (im2col == 0 && a.a_narrow)
+                                               ? uint32_t(TC_BM * a.a_narrow * 2)
+                                               : uint32_t(Cfg::A_BYTES);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const int t = u % ntiles;
+      int kb0, kb1;
+      split_range(u / ntiles, a.nsplit, KT, kb0, kb1);
+      const int m0 = mtile_of(a, t) * TC_BM;
+      const int n0 = (t % a.tiles_n) * BN;
+      int iw0 = 0, ih0 = 0, img = 0;
+      if (!GATHER && (im2col || fold == 2)) {
+        img = m0 / a.OHW;
+        const int rem = m0 - img * a.OHW;
+        const int oh = rem / a.OW;
+        ih0 = oh * a.stride;
+        iw0 = (rem - oh * a.OW) * a.stride;
+      }
+      // im2col (mode 1) counters at K block kb0: channel offset and filter tap
+      int c0 = 0, s2 = 0, r = 0;
+      if (!GATHER && im2col == 1 && kb0 > 0 && kb0 < kblocks) {
+        const int cpb = Cin >> 6;
+        const int tap = kb0 / cpb;
+        c0 = (kb0 - tap * cpb) << 6;
+        r = tap / Stap;
+        s2 = tap - r * Stap;
+      }
+      for (int kb = kb0; kb < kb1; ++kb) {
 #ifdef B2_TILE_TS
-          if (kb == kb0 && TS_DBG(a) == 2) tile_stamp(a, 5, (u - (int)blockIdx.x) / (int)gridDim.x);
+        if (kb == kb0 && TS_DBG(a) == 2 && lane == 0)
+          tile_stamp(a, 5, (u - (int)blockIdx.x) / (int)gridDim.x);
 #endif
-          mbar_wait(&empty[stage], phase ^ 1);
+        mbar_wait_u32(empty_lo + stage * 8, phase ^ 1);
 #ifdef B2_TILE_TS
-          if (kb == kb0 && TS_DBG(a) == 2) tile_stamp(a, 0, (u - (int)blockIdx.x) / (int)gridDim.x);
+        if (kb == kb0 && TS_DBG(a) == 2 && lane == 0)
+          tile_stamp(a, 0, (u - (int)blockIdx.x) / (int)gridDim.x);
 #endif
-          if (kb >= a.kblocks) {
-            const int j = kb - a.kblocks;
-            mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
-            if (a.fold_kind == 0) {
+        const uint32_t fb = full_lo + stage * 8;
+        const uint32_t dA = sA_lo + stage * Cfg::A_BYTES;
+        const uint32_t dB = sB_lo + stage * Cfg::B_BYTES;
+        if (elect_one()) {
+          if (kb >= kblocks) {
+            const int j = kb - kblocks;
+            mbar_arrive_expect_tx_u32(fb, Cfg::A_BYTES + Cfg::B_BYTES);
+            if (fold == 0) {
               // residual fold: A = res[m0:, n0 + j*64:], B = identity rows [0, BN)
-              tma_load_2d(sA + stage * Cfg::A_BYTES, &tmR, &full[stage], n0 + j * TC_BK, m0);
-              tma_load_2d(sB + stage * Cfg::B_BYTES, &tmI, &full[stage], j * TC_BK, 0);
+              tma_load_2d_u32(dA, &tmR, fb, n0 + j * TC_BK, m0);
+              tma_load_2d_u32(dB, &tmI, fb, j * TC_BK, 0);
             } else {
               // folded projection shortcut: A = its input x, B = its weights
-              if (a.fold_kind == 1) {
-                tma_load_2d(sA + stage * Cfg::A_BYTES, &tmR, &full[stage], j * TC_BK, m0);
-              } else {
-                const int im = m0 / a.OHW;
-                const int rem = m0 - im * a.OHW;
-                const int oh = rem / a.OW;
-                tma_load_im2col_4d(sA + stage * Cfg::A_BYTES, &tmR, &full[stage], j * TC_BK,
-                                   (rem - oh * a.OW) * a.stride, oh * a.stride, im, 0, 0);
-              }
-              tma_load_2d(sB + stage * Cfg::B_BYTES, &tmI, &full[stage], j * TC_BK, n0);
+              if (fold == 1)
+                tma_load_2d_u32(dA, &tmR, fb, j * TC_BK, m0);
+              else
+                tma_load_im2col_4d_u32(dA, &tmR, fb, j * TC_BK, iw0, ih0, img, 0, 0);
+              tma_load_2d_u32(dB, &tmI, fb, j * TC_BK, n0);
             }
           } else {
             if (GATHER) {
-              mbar_arrive_expect_tx(&full[stage], Cfg::B_BYTES);
-            } else if (a.a_im2col == 3) {
+              mbar_arrive_expect_tx_u32(fb, Cfg::B_BYTES);
+            } else if (im2col == 3) {
               // s2d stem: tile = output row (img, oh); K block kb = filter row-pair
-              mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
+              mbar_arrive_expect_tx_u32(fb, Cfg::A_BYTES + Cfg::B_BYTES);
               const int rt = m0 / TC_BM;
               const int im = rt / a.OH;
-              tma_load_4d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], 0, 0,
-                          rt - im * a.OH + kb, im);
-            } else if (a.a_im2col == 2) {
+              tma_load_4d_u32(dA, &tmA, fb, 0, 0, rt - im * a.OH + kb, im);
+            } else if (im2col == 2) {
               // 8 taps x (128 pixels x 8 channels); taps past R*S load tap 0
               // (finite data) against zero weights
-              mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
+              mbar_arrive_expect_tx_u32(fb, Cfg::A_BYTES + Cfg::B_BYTES);
               const int ntaps = a.R * a.S;
 #pragma unroll 1
               for (int j = 0; j < 8; ++j) {
                 int tap = kb * 8 + j;
                 if (tap >= ntaps) tap = 0;
-                const int r = tap / a.S;
-                const int s = tap - r * a.S;
-                tma_load_im2col_4d(sA + stage * Cfg::A_BYTES + j * 2048, &tmA, &full[stage], 0,
-                                   iw0, ih0, img, (uint16_t)s, (uint16_t)r);
+                const int rr = tap / a.S;
+                const int ss = tap - rr * a.S;
+                tma_load_im2col_4d_u32(dA + j * 2048, &tmA, fb, 0, iw0 - a.pad, ih0 - a.pad, img,
+                                       (uint16_t)ss, (uint16_t)rr);
               }
-            } else if (a.a_im2col) {
-              mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
-              const int tap = kb / cpb;
-              const int c0 = (kb - tap * cpb) << 6;
-              const int r = tap / a.S;
-              const int s = tap - r * a.S;
-              tma_load_im2col_4d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], c0, iw0, ih0,
-                                 img, (uint16_t)s, (uint16_t)r);
+            } else if (im2col) {
+              mbar_arrive_expect_tx_u32(fb, Cfg::A_BYTES + Cfg::B_BYTES);
+              tma_load_im2col_4d_u32(dA, &tmA, fb, c0, iw0 - a.pad, ih0 - a.pad, img,
+                                     (uint16_t)s2, (uint16_t)r);
             } else {
               // narrow K: the A box is a_narrow elements wide (no out-of-bounds fill)
-              mbar_arrive_expect_tx(&full[stage], (a.a_narrow ? TC_BM * a.a_narrow * 2
-                                                               : Cfg::A_BYTES) + Cfg::B_BYTES);
-              tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * TC_BK, m0);
+              mbar_arrive_expect_tx_u32(fb, a_bytes + Cfg::B_BYTES);
+              tma_load_2d_u32(dA, &tmA, fb, kb * TC_BK, m0);
             }
-            tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * TC_BK, n0);
+            tma_load_2d_u32(dB, &tmB, fb, kb * TC_BK, n0);
           }
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+        }
+        __syncwarp();
+        if ((c0 += TC_BK) >= Cin) {
+          c0 = 0;
+          if (++s2 == Stap) {
+            s2 = 0;
+            ++r;
           }
+        }
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
@@ -775,61 +798,79 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<BN>::THREADS,
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
-    if (lane == 0) {
-      const int cpb = a.C >> 6;
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = cid; t < ntiles; t += ncl) {
-        const int m0 = mtile_of(a, t) * (2 * TC_BM) + (int)rank * TC_BM;
-        const int n0 = (t % a.tiles_n) * BN;
-        const int nb = n0 + (int)rank * (BN / 2);          // this CTA's half of the weights
-        int iw0 = 0, ih0 = 0, img = 0;
-        if (a.a_im2col) {
-          img = m0 / a.OHW;
-          const int rem = m0 - img * a.OHW;
-          const int oh = rem / a.OW;
-          ih0 = oh * a.stride - a.pad;
-          iw0 = (rem - oh * a.OW) * a.stride - a.pad;
-        }
-        for (int kb = 0; kb < KT; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          const uint32_t fl = mapa_shared(&full[stage], 0);
-          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
-          uint8_t* dA = sA + stage * Cfg::A_BYTES;
-          uint8_t* dB = sB + stage * Cfg::B_BYTES;
-          if (kb >= a.kblocks) {
-            const int j = kb - a.kblocks;
-            if (a.fold_kind == 0) {   // residual x identity (this CTA's half of the rows)
-              tma_load_2d_pair(dA, &tmR, fl, n0 + j * TC_BK, m0);
-              tma_load_2d_pair(dB, &tmI, fl, j * TC_BK, (int)rank * (BN / 2));
-            } else {                  // folded projection shortcut: x (or strided x) x Wd
-              if (a.fold_kind == 1) {
-                tma_load_2d_pair(dA, &tmR, fl, j * TC_BK, m0);
-              } else {
-                const int im = m0 / a.OHW;
-                const int rem = m0 - im * a.OHW;
-                const int oh = rem / a.OW;
-                tma_load_im2col_4d_pair(dA, &tmR, fl, j * TC_BK, (rem - oh * a.OW) * a.stride,
-                                        oh * a.stride, im, 0, 0);
-              }
-              tma_load_2d_pair(dB, &tmI, fl, j * TC_BK, nb);
+    // The whole warp runs the loop converged and one elected lane issues:
+    // every value below derives from kernel parameters, blockIdx and loop
+    // counters (warp-uniform), so the TMA operands live in uniform registers.
+    // (A single-lane producer paid an ELECT/R2UR waterfall per TMA, two integer
+    // divisions and constant-bank reloads per K block, ~100 SASS per 512-clock
+    // K block: ncu showed it never waiting for a free ring slot while the MMA
+    // thread spun on full barriers — the producer paced the kernel.)  Per K
+    // block now: the empty wait, address adds, the loads, and im2col taps
+    // advanced as counters.
+    const int Cin = a.C;
+    const int Stap = a.S;
+    const int kblocks = a.kblocks;
+    const bool im2col = a.a_im2col != 0;
+    const int fold = a.fold_kind;
+    const int urank = (int)uniform_u32(rank);
+    const uint32_t full_cl = uniform_u32(mapa_shared(&full[0], 0));   // the leader's full[0]
+    const uint32_t full_lo = uniform_u32(smem_u32(&full[0]));
+    const uint32_t empty_lo = uniform_u32(smem_u32(&empty[0]));
+    const uint32_t sA_lo = uniform_u32(smem_u32(sA)), sB_lo = uniform_u32(smem_u32(sB));
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = cid; t < ntiles; t += ncl) {
+      const int m0 = mtile_of(a, t) * (2 * TC_BM) + urank * TC_BM;
+      const int n0 = (t % a.tiles_n) * BN;
+      const int nb = n0 + urank * (BN / 2);          // this CTA's half of the weights
+      int iw0 = 0, ih0 = 0, img = 0;
+      if (im2col || fold == 2) {
+        img = m0 / a.OHW;
+        const int rem = m0 - img * a.OHW;
+        const int oh = rem / a.OW;
+        ih0 = oh * a.stride;
+        iw0 = (rem - oh * a.OW) * a.stride;
+      }
+      int c0 = 0, s2 = 0, r = 0;                      // im2col: channel block, filter tap
+      for (int kb = 0; kb < KT; ++kb) {
+        mbar_wait_u32(empty_lo + stage * 8, phase ^ 1);
+        const uint32_t fl = full_cl + stage * 8;
+        const uint32_t dA = sA_lo + stage * Cfg::A_BYTES;
+        const uint32_t dB = sB_lo + stage * Cfg::B_BYTES;
+        if (elect_one()) {
+          if (urank == 0) mbar_arrive_expect_tx_u32(full_lo + stage * 8, 2 * Cfg::STAGE_BYTES);
+          if (kb >= kblocks) {
+            const int j = kb - kblocks;
+            if (fold == 0) {   // residual x identity (this CTA's half of the rows)
+              tma_load_2d_pair_u32(dA, &tmR, fl, n0 + j * TC_BK, m0);
+              tma_load_2d_pair_u32(dB, &tmI, fl, j * TC_BK, urank * (BN / 2));
+            } else {           // folded projection shortcut: x (or strided x) x Wd
+              if (fold == 1)
+                tma_load_2d_pair_u32(dA, &tmR, fl, j * TC_BK, m0);
+              else
+                tma_load_im2col_4d_pair_u32(dA, &tmR, fl, j * TC_BK, iw0, ih0, img, 0, 0);
+              tma_load_2d_pair_u32(dB, &tmI, fl, j * TC_BK, nb);
             }
           } else {
-            if (a.a_im2col) {
-              const int tap = kb / cpb;
-              const int c0 = (kb - tap * cpb) << 6;
-              const int r = tap / a.S;
-              const int s2 = tap - r * a.S;
-              tma_load_im2col_4d_pair(dA, &tmA, fl, c0, iw0, ih0, img, (uint16_t)s2, (uint16_t)r);
-            } else {
-              tma_load_2d_pair(dA, &tmA, fl, kb * TC_BK, m0);
-            }
-            tma_load_2d_pair(dB, &tmB, fl, kb * TC_BK, nb);
+            if (im2col)
+              tma_load_im2col_4d_pair_u32(dA, &tmA, fl, c0, iw0 - a.pad, ih0 - a.pad, img,
+                                          (uint16_t)s2, (uint16_t)r);
+            else
+              tma_load_2d_pair_u32(dA, &tmA, fl, kb * TC_BK, m0);
+            tma_load_2d_pair_u32(dB, &tmB, fl, kb * TC_BK, nb);
           }
-          if (++stage == ST) {
-            stage = 0;
-            phase ^= 1;
+        }
+        __syncwarp();
+        if ((c0 += TC_BK) >= Cin) {
+          c0 = 0;
+          if (++s2 == Stap) {
+            s2 = 0;
+            ++r;
           }
+        }
+        if (++stage == ST) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }

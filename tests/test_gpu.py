@@ -101,6 +101,7 @@ def test_batch_invariance_and_determinism_at_full_size(gpu_required, monkeypatch
     pl = P.decode(blob)
     big = 256 if name == "resnet50" else 128
     x = plan_ref.make_inputs(pl, big, 5)
+    monkeypatch.setenv("B2_DEV", "1")         # kernel-selection knobs honoured
     for split in ("0", "1"):
         monkeypatch.setenv("B2_SPLIT", split)
         monkeypatch.setenv("B2_PAIR", split)
