@@ -322,7 +322,11 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 // issues from one elected lane.
 B2_DEV int warp_index_uniform() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
 B2_DEV uint32_t uniform_u32(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
+// elect.sync names the full warp: the warp is reconverged first (lanes leave
+// an mbarrier poll loop in different iterations, and an elect.sync over a split
+// warp elects one lane per fragment — two producers arriving on one barrier).
 B2_DEV bool elect_one() {
+  __syncwarp();
   uint32_t pred;
   asm volatile(
       "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
