@@ -185,6 +185,48 @@ def closed_loop_load(endpoint: str, make_batch: Callable[[int], np.ndarray], *,
     return res
 
 
+def device_loop_load(endpoint: str, batch: int, *, requests_per_call: int = 20,
+                     stop: Optional[threading.Event] = None, n_calls: Optional[int] = None,
+                     e2e: bool = True, timeout_s: float = 60.0) -> LoadResult:
+    """A GPU-bound online-serving load: the worker runs back-to-back requests
+    of ``batch`` samples (``bench`` frames; with ``e2e`` every request copies
+    its inputs host->device from pinned memory and its outputs back, as a
+    serving process would), each request timed on the device with CUDA
+    events.  Request latencies therefore include any time the GPU spent on
+    another process's kernels in between — what a co-located profiling job
+    costs the service.  Completion instants are mapped to the host clock from
+    the reply time (the binary-frame clients above measure the whole RPC
+    instead, which on a loopback socket is dominated by host copies)."""
+    if n_calls is None and stop is None:
+        raise ValueError("give n_calls or a stop event")
+    from .profiler.clients import make_client
+    host, port = split_endpoint(endpoint)
+    cli = make_client("grpc-style", host, port, timeout_s)
+    res = LoadResult()
+    res.t0 = time.monotonic()
+    k = 0
+    try:
+        while (n_calls is None or k < n_calls) and not (stop is not None and stop.is_set()):
+            reply = cli.call({"kind": "bench", "batch": batch, "n": requests_per_call,
+                              "warmup": 0, "seed": k, "e2e": e2e})
+            t_r = time.monotonic()
+            if not reply or not reply.get("ok"):
+                res.failed += requests_per_call
+                raise RequestFailure(f"serving bench failed: {(reply or {}).get('error')}")
+            lat, comp = reply["latencies_ms"], reply["completions_ms"]
+            end = float(comp[-1])
+            for l_ms, c_ms in zip(lat, comp):
+                w = t_r - (end - float(c_ms)) / 1e3
+                res.latencies_ms.append(float(l_ms))
+                res.wall_done.append(w)
+                res.completions_ms.append((w - res.t0) * 1e3)
+                res.service_ms.append(float(l_ms))
+            k += 1
+    finally:
+        cli.close()
+    return res
+
+
 class DynamicBatcher:
     """Merge concurrent requests into one forward.
 

@@ -183,23 +183,25 @@ def fold_units(job: ProfilingJob, measured: list) -> list[ProfilingResult]:
     return out
 
 
-def partitioned_sweep(jobs: list[ProfilingJob], rank: int, world: int, measure,
-                      cost_fn: Callable[[ProfilingJob, Cell], float],
-                      setup_s: Callable[[ProfilingJob], float] | None = None) -> list:
-    """The torchrun-style C4 sweep: one process per GPU, no data-path
-    collective.  Heavy cells are request-sharded (``plan_shards``), the work
-    units are partitioned by the setup-aware LPT (a rank pays a model's load
-    once), rank r measures its units locally with ``measure(job, unit) ->
-    LatencySamples``, and only the samples documents are gathered to rank 0,
-    which folds them into ProfilingResults (returned on rank 0; [] elsewhere).
-    Every rank computes the same partition (deterministic)."""
+def partition_units(jobs: list[ProfilingJob], world: int,
+                    cost_fn: Callable[[ProfilingJob, Cell], float],
+                    setup_s: Callable[[ProfilingJob], float] | None = None) -> list[list]:
+    """The static partition of a torchrun-style sweep: heavy cells
+    request-sharded (``plan_shards``), then every remaining work unit
+    (job, cell-or-shard) placed by the setup-aware LPT (a rank pays a model's
+    load once).  Deterministic, so every rank computes the same one."""
     plan_shards(jobs, world, cost_fn)
     units = [(j, u) for j in jobs for u in j.remaining_units()]
-    parts = lpt_partition(units, lambda ju: cost_fn(*ju), world,
-                          group=(lambda ju: ju[0].id) if setup_s else None,
-                          setup=(lambda jid: setup_s(next(j for j in jobs if j.id == jid)))
-                          if setup_s else None)
-    mine = parts[rank]
+    by_id = {j.id: j for j in jobs}
+    return lpt_partition(units, lambda ju: cost_fn(*ju), world,
+                         group=(lambda ju: ju[0].id) if setup_s else None,
+                         setup=(lambda jid: setup_s(by_id[jid])) if setup_s else None)
+
+
+def run_units(jobs: list[ProfilingJob], mine: list, rank: int, world: int, measure) -> list:
+    """Measure this rank's units (``measure(job, unit) -> LatencySamples``)
+    and gather only the samples documents to rank 0, which folds them into
+    ProfilingResults (returned on rank 0; [] elsewhere)."""
     docs = []
     for job, unit in mine:
         samp = measure(job, unit)
@@ -218,6 +220,15 @@ def partitioned_sweep(jobs: list[ProfilingJob], rank: int, world: int, measure,
                   if jid == job.id]
         out += fold_units(job, mine_j)
     return out
+
+
+def partitioned_sweep(jobs: list[ProfilingJob], rank: int, world: int, measure,
+                      cost_fn: Callable[[ProfilingJob, Cell], float],
+                      setup_s: Callable[[ProfilingJob], float] | None = None) -> list:
+    """The torchrun-style C4 sweep: one process per GPU, no data-path
+    collective — ``partition_units`` then ``run_units`` on this rank's share."""
+    mine = partition_units(jobs, world, cost_fn, setup_s)[rank]
+    return run_units(jobs, mine, rank, world, measure)
 
 
 class BusyLedger:

@@ -173,3 +173,24 @@ def test_oversized_json_frame_rejected_from_header(server):
     s.settimeout(5)
     assert s.recv(16) == b""          # the worker dropped the connection
     s.close()
+
+
+class BenchPlan(FakePlan):
+    def bench(self, batch, n, warm, seed, e2e=False):
+        lat = np.full(n, 0.5)
+        return lat, np.cumsum(lat)
+
+    def device_bytes(self):
+        return 1 << 20
+
+
+def test_device_loop_load_maps_device_completions_to_wall_time(server):
+    from paper_2006_05096_b200.online import device_loop_load
+    ep = server(FakeExecutor(BenchPlan()))
+    res = device_loop_load(ep, 16, requests_per_call=10, n_calls=3)
+    assert len(res.latencies_ms) == 30 and all(v == 0.5 for v in res.latencies_ms)
+    assert res.wall_done == sorted(res.wall_done) or len(set(res.wall_done)) > 1
+    assert res.p(99) == 0.5
+    stop = threading.Event()
+    stop.set()
+    assert len(device_loop_load(ep, 16, stop=stop).latencies_ms) == 0

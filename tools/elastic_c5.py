@@ -1,6 +1,14 @@
 """C5 elastic evaluation on this box (BASELINE configs[4]): a ResNet-50 bf16
-online-serving load (closed-loop binary-predict clients, TCP_NODELAY,
-worker-side dynamic batching) holds a p99 SLO while profiling jobs arrive.
+online-serving load holds a p99 SLO while profiling jobs arrive.
+
+The serving load (``--load device``, default) is GPU-bound: back-to-back
+requests of ``--serve-batch`` images inside the serving worker, each copying
+its inputs host->device from pinned memory and its outputs back, timed on
+the device (online.device_loop_load) — request latency includes any time the
+GPU gives another process.  ``--load binary`` drives closed-loop binary
+predict clients over TCP instead (online.closed_loop_load); on one host that
+load is bound by Python socket copies of 0.6 MB/image and keeps the GPU ~8%
+busy, so it cannot show interference.
 
 Three phases on gpu:0, serving load running throughout phases 1-3:
   1. serving alone                          -> the p99 baseline, SLO = slo_x * that
@@ -35,7 +43,8 @@ from paper_2006_05096_b200 import converter, zoo  # noqa: E402
 from paper_2006_05096_b200.controller import ControllerConfig  # noqa: E402
 from paper_2006_05096_b200.dispatcher import Dispatcher, b200_template  # noqa: E402
 from paper_2006_05096_b200.hub import Hub, TensorSpec  # noqa: E402
-from paper_2006_05096_b200.online import closed_loop_load, slo_report  # noqa: E402
+from paper_2006_05096_b200.online import (closed_loop_load, device_loop_load,  # noqa: E402
+                                          slo_report)
 from paper_2006_05096_b200.profiler.sweep import JobStore, Profiler  # noqa: E402
 from paper_2006_05096_b200.profiler.types import ProfilingJob, SweepSpec  # noqa: E402
 from paper_2006_05096_b200.sweeprun import CellRunner, ControllerSweep, nvml_hooks  # noqa: E402
@@ -59,14 +68,15 @@ def main() -> int:
     ap.add_argument("--phase-s", type=float, default=4.0)
     ap.add_argument("--slo-x", type=float, default=1.5)
     ap.add_argument("--requests", type=int, default=100)
+    ap.add_argument("--load", choices=["device", "binary"], default="device")
     args = ap.parse_args()
 
     hub = Hub()
     prov = NvmlProvider()
     tel = Telemetry(prov)
     tel.sample_devices()
-    disp = Dispatcher(hub, {"b200": b200_template(extra_args=("--max-batch", "128",
-                                                              "--batch-timeout-ms", "1.0"))},
+    extra = ("--max-batch", "128", "--batch-timeout-ms", "1.0") if args.load == "binary" else ()
+    disp = Dispatcher(hub, {"b200": b200_template(extra_args=extra)},
                       Path(tempfile.mkdtemp()), tel.device_ids)
     tel.instance_pid_resolver = disp.pid_of
     tel.instance_device_resolver = disp.device_of
@@ -80,14 +90,18 @@ def main() -> int:
     svc = disp.dispatch(serve_var, "gpu:0", "b200", "grpc-style")
     rng = np.random.default_rng(0)
     batches = [rng.standard_normal((args.serve_batch, 3 * 224 * 224), dtype=np.float32)
-               for _ in range(args.clients)]
+               for _ in range(args.clients if args.load == "binary" else 0)]
     stop = threading.Event()
     load = {}
     util = []
 
     def serve_load():
-        load["res"] = closed_loop_load(svc.endpoint, lambda i: batches[i],
-                                       concurrency=args.clients, stop=stop, warmup_requests=3)
+        if args.load == "device":
+            load["res"] = device_loop_load(svc.endpoint, args.serve_batch, stop=stop)
+        else:
+            load["res"] = closed_loop_load(svc.endpoint, lambda i: batches[i],
+                                           concurrency=args.clients, stop=stop,
+                                           warmup_requests=3)
 
     def sampler():
         while not stop.is_set():
@@ -159,9 +173,11 @@ def main() -> int:
             break
     u_serv = [u for t, u in util if t_start + 0.5 <= t < t1]
     out = {
-        "config": f"C5 elastic: ResNet-50 bf16 serving (b={args.serve_batch}, {args.clients} "
-                  f"closed-loop binary clients, worker dynamic batching <= 128) on gpu:0; "
-                  f"profiling jobs {prof_models} x b in {{1,16,64,256}}, n={args.requests}",
+        "config": f"C5 elastic: ResNet-50 bf16 serving on gpu:0, b={args.serve_batch}, load "
+                  + ("device (back-to-back requests with pinned H2D/D2H, CUDA-event timed)"
+                     if args.load == "device" else
+                     f"{args.clients} closed-loop binary clients, worker dynamic batching <= 128")
+                  + f"; profiling jobs {prof_models} x b in {{1,16,64,256}}, n={args.requests}",
         "slo_ms": round(slo, 3), "slo_rule": f"{args.slo_x} x p99 of serving alone",
         "windows": slo_report(res, slo, windows),
         "nvml_util_serving_alone": {"median": float(np.median(u_serv)) if u_serv else None,
