@@ -35,11 +35,15 @@ def load(path):
 def main():
     src, out = sys.argv[1], sys.argv[2]
     L = load(src)
-    starts = [i for i, d in enumerate(L) if "input_pack" in d["name"]]
+    # one forward = from the last input-packing launch (images) or token pack (BERT)
+    first = sys.argv[3] if len(sys.argv) > 3 else None
+    starts = [i for i, d in enumerate(L)
+              if (first and first in d["name"]) or (not first and ("input_pack" in d["name"]
+                                                                     or "tokens_pack" in d["name"]))]
     fwd = L[starts[-1]:]
     pk = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
     tf_peak, hbm_peak = pk["bf16_tflops"], pk["hbm_gbs"]
-    lines = [f"ncu --metrics (cold cache, serialised) of one ResNet-50 bf16 b=256 forward: "
+    lines = [f"ncu --metrics (cold cache, serialised) of one forward: "
              f"{src}\npeaks: bf16 {tf_peak} TFLOP/s burst, HBM {hbm_peak} GB/s "
              f"(MEASURED_PEAKS.json)\n",
              f"{'#':>2} {'kernel':34s} {'us':>7s} {'tensor%':>7s} {'DRAM MB':>8s} {'GB/s':>6s} "
