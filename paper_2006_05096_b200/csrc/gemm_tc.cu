@@ -107,51 +107,19 @@ B2_DEV int mtile_of(const TcArgs& a, int t) {
 // Tiles t = t0, t0 + tstep, ... < ntiles; tile t covers rows
 // (t / tiles_n) * mstride + mofs.  `tempty_remote` != 0: signal accumulator
 // release on the CTA-pair leader's barrier (cluster address) instead of ours.
-// Residual tiles by TMA (a.res_tma): each epilogue warp owns max(2, BN/64)
-// 2 KB slots; the 32 x 32 residual boxes of its chunks of tile i+1 are loaded
-// into them (64B swizzle, the staging layout) as soon as tile i's stores have
-// read the slots out, so the loads fly during tile i+1's mainloop.  Chunk j
-// reads its residual from slot j and stages its output in the same slot.
-// Replaces the identity-MMA residual fold (2x the MMA K and identity tiles
-// through the L2->SM path) and the register prefetch one chunk ahead (a DRAM
-// round trip exposed per chunk).
-B2_DEV constexpr int epi_slots(int bn) { return bn / 64 > 2 ? bn / 64 : 2; }
-
-template <int BN>
-B2_DEV void epi_res_issue(const TcArgs& a, const CUtensorMap& tmR, uint8_t* obuf, uint64_t* rbar,
-                          int t, int mstride, int mofs, int lg, int eh, int lane) {
-  if (lane == 0) {
-    bulk_wait_read<0>();              // the previous tile's stores are out of the slots
-    fence_proxy_async_smem();
-    const int m0 = mtile_of(a, t) * mstride + mofs;
-    const int n0 = (t % a.tiles_n) * BN;
-    int nch = 0;
-    for (int c = eh * 32; c < BN && n0 + c < a.N; c += 64) ++nch;
-    mbar_arrive_expect_tx(rbar, (uint32_t)nch * 2048u);
-    int j = 0;
-    for (int c = eh * 32; c < BN && n0 + c < a.N; c += 64, ++j)
-      tma_load_2d(obuf + j * 2048, &tmR, rbar, n0 + c, m0 + lg * 32);
-  }
-  __syncwarp();
-}
-
 template <int BN, int ACT>
-B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, const CUtensorMap& tmR,
-                    uint8_t* sEpi, uint64_t* rbar_all, uint64_t* tfull,
+B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint64_t* tfull,
                     uint64_t* tempty, uint32_t tmem_base, int ntiles, int lg, int ew, int eh,
                     int lane, int t0, int tstep, int mstride, int mofs, uint32_t tempty_remote) {
-  const bool res_tma = a.res_tma != 0;
-  const bool has_res = a.res != nullptr && !res_tma;
+  const bool has_res = a.res != nullptr;
   int it = 0;
   // 32-column chunks split between the two warps of each TMEM lane
   // quadrant (chunk parity = warp half).  Per chunk: tcgen05.ld.x32, +bias,
-  // +residual (TMA-prefetched tile, or registers one chunk ahead), act, bf16
-  // pack into a 64B-swizzled 32x32 staging tile, per-warp TMA store.
-  uint8_t* obuf = sEpi + ew * (res_tma ? epi_slots(BN) * 2048 : 4096);
-  uint64_t* rbar = rbar_all + ew;
+  // +residual (prefetched one chunk ahead), act, bf16 pack into a
+  // 64B-swizzled 32x32 staging tile, per-warp TMA store.
+  uint8_t* obuf = sEpi + ew * 4096;
   uint32_t oi = 0;
   const uint32_t swz = (lane >> 1) & 3;
-  if (res_tma && t0 < ntiles) epi_res_issue<BN>(a, tmR, obuf, rbar, t0, mstride, mofs, lg, eh, lane);
   for (int t = t0; t < ntiles; t += tstep, ++it) {
     const int as = it & 1;
     const uint32_t aph = (it >> 1) & 1;
@@ -182,21 +150,13 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, const CUtensorMap& 
 #ifdef B2_TILE_TS
     if (ew == 0 && lane == 0) tile_stamp(a, 3, it);
 #endif
-    if (res_tma) mbar_wait(rbar, it & 1);
-    __syncwarp();                       // lanes leave the polls apart; tcgen05.ld is .aligned
     const uint32_t taddr = tmem_base + (uint32_t(lg * 32) << 16) + as * BN;
-    int jc = 0;
 #pragma unroll 1
-    for (int c = eh * 32; c < BN && n0 + c < a.N; c += 64, ++jc) {   // ragged N: skip empty chunks
+    for (int c = eh * 32; c < BN && n0 + c < a.N; c += 64) {   // ragged N: skip empty chunks
       uint32_t r[32];
       tmem_ld_32x32b_x32(taddr + c, r);
       uint4 rcur[4];
-      uint8_t* rslot = obuf + jc * 2048 + lane * 64;   // res_tma: this chunk's slot, our row
-      if (res_tma) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          rcur[q] = *reinterpret_cast<const uint4*>(rslot + ((q ^ swz) << 4));
-      } else if (has_res) {
+      if (has_res) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) rcur[q] = rnext[q];
         if (c + 64 < BN) {
@@ -224,7 +184,7 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, const CUtensorMap& 
       float v[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + bv[j];
-      if (has_res || res_tma) {
+      if (has_res) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) add_bf16x8(v + 8 * q, rcur[q]);
       }
@@ -234,9 +194,9 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, const CUtensorMap& 
 #pragma unroll
         for (int j = 0; j < 16; ++j) gelu_erf2(v[2 * j], v[2 * j + 1]);
       }
-      if (!res_tma && lane == 0 && EPI_DBG(a) != 4 && EPI_DBG(a) != 5) bulk_wait_read<1>();
+      if (lane == 0 && EPI_DBG(a) != 4 && EPI_DBG(a) != 5) bulk_wait_read<1>();
       __syncwarp();
-      uint8_t* sbuf = res_tma ? obuf + jc * 2048 : obuf + (oi & 1) * 2048;
+      uint8_t* sbuf = obuf + (oi & 1) * 2048;
       uint8_t* orow = sbuf + lane * 64;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -271,8 +231,6 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, const CUtensorMap& 
       if (ew == 0) tile_stamp(a, 4, it);
 #endif
     }
-    if (res_tma && t + tstep < ntiles)
-      epi_res_issue<BN>(a, tmR, obuf, rbar, t + tstep, mstride, mofs, lg, eh, lane);
   }
   if (lane == 0) bulk_wait<0>();
 }
@@ -292,13 +250,11 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
   uint8_t* sEpi = sB + STAGES * Cfg::B_BYTES;
-  const int epi_bytes = a.res_tma ? TC_EPI_WARPS * epi_slots(BN) * 2048 : TC_EPI_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + epi_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + TC_EPI_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* rbar = tempty + 2;          // [TC_EPI_WARPS] residual tiles landed (res_tma)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + TC_EPI_WARPS);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = warp_index_uniform();
   const int lane = threadIdx.x & 31;
@@ -328,13 +284,12 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], TC_EPI_WARPS);
     }
-    for (int i = 0; i < TC_EPI_WARPS; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
     if (!GATHER) tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    if (a.res_kblocks || a.res_tma) {
+    if (a.res_kblocks) {
       tma_prefetch_desc(&tmR);
       tma_prefetch_desc(&tmI);
     }
@@ -572,11 +527,11 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
       }
     } else if (BN >= 32 && a.tma_epi) {
       switch (a.act) {
-        case ACT_RELU: epi_tma<BN, ACT_RELU>(a, tmO, tmR, sEpi, rbar, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, blockIdx.x, gridDim.x, TC_BM, 0, 0u); break;
-        case ACT_RELU6: epi_tma<BN, ACT_RELU6>(a, tmO, tmR, sEpi, rbar, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, blockIdx.x, gridDim.x, TC_BM, 0, 0u); break;
-        case ACT_GELU: epi_tma<BN, ACT_GELU>(a, tmO, tmR, sEpi, rbar, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, blockIdx.x, gridDim.x, TC_BM, 0, 0u); break;
-        case ACT_TANH: epi_tma<BN, ACT_TANH>(a, tmO, tmR, sEpi, rbar, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, blockIdx.x, gridDim.x, TC_BM, 0, 0u); break;
-        default: epi_tma<BN, ACT_NONE>(a, tmO, tmR, sEpi, rbar, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, blockIdx.x, gridDim.x, TC_BM, 0, 0u); break;
+        case ACT_RELU: epi_tma<BN, ACT_RELU>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, blockIdx.x, gridDim.x, TC_BM, 0, 0u); break;
+        case ACT_RELU6: epi_tma<BN, ACT_RELU6>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, blockIdx.x, gridDim.x, TC_BM, 0, 0u); break;
+        case ACT_GELU: epi_tma<BN, ACT_GELU>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, blockIdx.x, gridDim.x, TC_BM, 0, 0u); break;
+        case ACT_TANH: epi_tma<BN, ACT_TANH>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, blockIdx.x, gridDim.x, TC_BM, 0, 0u); break;
+        default: epi_tma<BN, ACT_NONE>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, blockIdx.x, gridDim.x, TC_BM, 0, 0u); break;
       }
     } else {
       // direct path (narrow tiles / N not a multiple of 8): 16-byte stores
@@ -784,16 +739,6 @@ struct Tc2Cfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + TC_EPI_BYTES + 1024 + TC_BAR_BYTES;
 };
 
-// Ring depth and dynamic smem of one launch: the epilogue region grows to
-// max(2, BN/64) slots per warp when the residual arrives by TMA.
-static int tc_epi_bytes(int bn, bool res_tma) {
-  return res_tma ? TC_EPI_WARPS * epi_slots(bn) * 2048 : TC_EPI_BYTES;
-}
-static int tc_fit_stages(int stage_bytes, int epi_bytes, int cap) {
-  int st = (TC_SMEM_MAX - epi_bytes - 1024 - TC_BAR_BYTES) / stage_bytes;
-  return st > cap ? cap : st;
-}
-
 template <int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<BN>::THREADS, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -802,20 +747,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<BN>::THREADS,
                     const __grid_constant__ CUtensorMap tmR,
                     const __grid_constant__ CUtensorMap tmI, const TcArgs a) {
   using Cfg = Tc2Cfg<BN>;
-  const int ST = a.stages;              // host: the most that fit next to the epilogue slots
+  constexpr int ST = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + ST * Cfg::A_BYTES;
   uint8_t* sEpi = sB + ST * Cfg::B_BYTES;
-  const int epi_bytes = a.res_tma ? TC_EPI_WARPS * epi_slots(BN) * 2048 : TC_EPI_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + epi_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + TC_EPI_BYTES);
   uint64_t* empty = full + ST;
   uint64_t* tfull = empty + ST;
   uint64_t* tempty = tfull + 2;
-  uint64_t* rbar = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + TC_EPI_WARPS);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = warp_index_uniform();
   const int lane = threadIdx.x & 31;
@@ -833,13 +776,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<BN>::THREADS,
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 2 * TC_EPI_WARPS);
     }
-    for (int i = 0; i < TC_EPI_WARPS; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    if (a.res_kblocks || a.res_tma) {
+    if (a.res_kblocks) {
       tma_prefetch_desc(&tmR);
       tma_prefetch_desc(&tmI);
     }
@@ -969,7 +911,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<BN>::THREADS,
     const uint32_t trem = rank == 0 ? 0u : mapa_shared(&tempty[0], 0);
     switch (a.act) {
 #define B2_EPI2(ACTV)                                                                            \
-  epi_tma<BN, ACTV>(a, tmO, tmR, sEpi, rbar, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, cid, ncl, \
+  epi_tma<BN, ACTV>(a, tmO, sEpi, tfull, tempty, tmem_base, ntiles, lg, ew, eh, lane, cid, ncl, \
                     2 * TC_BM, (int)rank * TC_BM, trem)
       case ACT_RELU: B2_EPI2(ACT_RELU); break;
       case ACT_RELU6: B2_EPI2(ACT_RELU6); break;
@@ -1000,17 +942,14 @@ static cudaError_t launch_bn(TcArgs a, const CUtensorMap& ta, const CUtensorMap&
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int epi = tc_epi_bytes(BN, a.res_tma != 0);
-  const int maxst = tc_fit_stages(Cfg::STAGE_BYTES, epi, 8);
-  if (a.stages <= 0 || a.stages > maxst) a.stages = maxst;
-  const int smem = a.stages * Cfg::STAGE_BYTES + epi + 1024 + TC_BAR_BYTES;
+  if (a.stages <= 0 || a.stages > Cfg::MAX_STAGES) a.stages = Cfg::MAX_STAGES;
   const int units = a.tiles_m * a.tiles_n * a.nsplit;
   const int grid = units < num_sms ? units : num_sms;
-  return launch_pdl(kern, dim3(grid), dim3(Cfg::THREADS), smem, st, ta, tb, to, tr, ti, a);
+  return launch_pdl(kern, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, ta, tb, to, tr, ti, a);
 }
 
 template <int BN>
@@ -1022,16 +961,14 @@ static cudaError_t launch_pair(TcArgs a, const CUtensorMap& ta, const CUtensorMa
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int epi = tc_epi_bytes(BN, a.res_tma != 0);
-  a.stages = tc_fit_stages(Cfg::STAGE_BYTES, epi, 10);
-  const int smem = a.stages * Cfg::STAGE_BYTES + epi + 1024 + TC_BAR_BYTES;
   const int tiles = a.tiles_m * a.tiles_n;
   const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  return launch_pdl(kern, dim3(2 * pairs), dim3(Cfg::THREADS), smem, st, ta, tb, to, tr, ti, a);
+  return launch_pdl(kern, dim3(2 * pairs), dim3(Cfg::THREADS), Cfg::SMEM, st, ta, tb, to, tr, ti,
+                    a);
 }
 
 // CTA-pair launch: a.tiles_m counts 256-row pair tiles; tb / ti boxes are BN/2 rows.

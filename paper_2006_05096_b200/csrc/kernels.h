@@ -49,8 +49,6 @@ struct TcArgs {
   int ds_H, ds_W;       // fold_kind 2: shortcut input geometry (uses OW, OHW, stride too)
   int res_kblocks;      // >0: residual folded into the MMA as [A | res] x [W | I]^T;
                         // BN/64 extra K blocks per tile, A from tmR, B from the identity
-  int res_tma;          // 1: residual tiles TMA-loaded by the epilogue warps (tmR = residual,
-                        // 32 x 32 boxes, 64B swizzle); `res` must be set as well
 };
 
 // ---- banded implicit-GEMM conv (conv_band.cu) --------------------------------

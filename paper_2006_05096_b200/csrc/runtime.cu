@@ -266,7 +266,6 @@ struct BatchState {
   std::vector<CUtensorMap> tmO;    // per layer (tc): output, 32x32 box, 64B swizzle
   std::vector<CUtensorMap> tmR;    // per layer (tc, residual fold): residual as an A operand
   std::vector<char> fold;          // per layer: residual folded into the MMA
-  std::vector<char> res_tma;       // per layer: residual tiles TMA-loaded by the epilogue (tmR)
   std::vector<char> a_narrow;      // per layer: A box width for K <= 32 (0 = 64)
   std::vector<CUtensorMap> tmI;    // per layer: identity [256 x 256] (box rows = BN) for the fold
   std::vector<char> band;          // per layer: banded implicit-GEMM conv (conv_band.cu)
@@ -312,8 +311,6 @@ struct b2_plan {
   int launches = 0;
   int epi_mode = 0;          // B2_EPI_MODE: 0 TMA-store epilogue, 1 drain-only, 2 direct stores
   int fold_max_k = 1024;     // B2_FOLD_MAX_K: fold residuals into the MMA when K <= this
-  bool use_res_tma = true;   // B2_RES_TMA=0 -> identity-MMA residual fold instead of the
-                             // TMA-prefetched epilogue residual (GEMM / CTA-pair GEMM)
   bool use_im2col = true;    // B2_IM2COL=0 -> cp.async gather for C % 64 == 0 convs
   bool use_s2d = true;       // B2_S2D=0 -> stems on the cp.async gather path
   bool im2col8 = false;      // B2_IM2COL8=1 -> 8-channel-tap im2col TMA for C == 8 stems
@@ -950,11 +947,10 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
             a.OHW = q[12] * q[13];
             a.stride = q[10];
           }
-          a.res_tma = S.res_tma[li];
           if (S.pair[li]) {
             a.tiles_m = (int)((M + 255) / 256);
             CK(tc_gemm2_launch(a, bn, S.tmA[li], S.tmB[li], S.tmO[li],
-                               (S.fold[li] || S.res_tma[li]) ? S.tmR[li] : S.tmO[li],
+                               S.fold[li] ? S.tmR[li] : S.tmO[li],
                                S.fold[li] ? S.tmI[li] : S.tmO[li], pl->num_sms, st));
           } else if (S.split[li] > 1) {
             a.nsplit = S.split[li];
@@ -969,7 +965,7 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
             ++launches;
           } else {
             CK(tc_gemm_launch(a, bn, L.gather, L.gather ? S.tmB[li] : S.tmA[li], S.tmB[li],
-                              S.tmO[li], (S.fold[li] || S.res_tma[li]) ? S.tmR[li] : S.tmO[li],
+                              S.tmO[li], S.fold[li] ? S.tmR[li] : S.tmO[li],
                               S.fold[li] ? S.tmI[li] : S.tmO[li], pl->num_sms, st));
           }
         } else {
@@ -1311,7 +1307,6 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
   S.tmO.resize(pl->layers.size());
   S.tmR.resize(pl->layers.size());
   S.fold.assign(pl->layers.size(), 0);
-  S.res_tma.assign(pl->layers.size(), 0);
   S.a_narrow.assign(pl->layers.size(), 0);
   S.tmI.resize(pl->layers.size());
   S.band.assign(pl->layers.size(), 0);
@@ -1377,8 +1372,7 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     const int res_in = conv ? p[15] : p[8];
     const int ds_kb = L.ds_op >= 0 ? pl->layers[L.ds_op].kpad / 64 : 0;   // folded shortcut K
     bool pair_ok = false;
-    int bn = tc_pick_config(M, N, L.kpad / 64 + ds_kb,
-                            res_in >= 0 && L.K <= pl->fold_max_k && !pl->use_res_tma,
+    int bn = tc_pick_config(M, N, L.kpad / 64 + ds_kb, res_in >= 0 && L.K <= pl->fold_max_k,
                             pl->num_sms, pair_allowed, &pair_ok);
     // Memory-bound shapes (one K block, or im2col A that each extra N tile
     // re-gathers) want the widest tile: measured 56x56x64->256 128 -> 115 us,
@@ -1449,18 +1443,6 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
                                  (uint64_t)D.kpad * 2, bbox))
         return fail(B2_ERR_CUDA, "layer %zu: folded shortcut tensor maps rejected", li);
       S.fold[li] = q[10] == 1 ? 2 : 3;
-    } else if (res_t >= 0 && pl->use_res_tma) {
-      // The residual is added in the epilogue, (acc + bias) + res in fp32, on
-      // every path and batch size (the identity-MMA fold rounds differently,
-      // which broke batch invariance between fold and non-fold tiles): tiles
-      // >= 64 wide take it through TMA into the staging slots, narrower ones
-      // by register prefetch; split-K adds it in its finalize pass.
-      if (bn >= 64 && N % 8 == 0 && S.split[li] == 1 && pl->epi_mode == 0) {
-        if (!make_tmap_bf16(&S.tmR[li], S.act[res_t], (uint64_t)M, (uint64_t)N, (uint64_t)N * 2,
-                            32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
-          return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeTiled(residual) failed", li);
-        S.res_tma[li] = 1;
-      }
     } else if (res_t >= 0 && bn >= 32 && N % 8 == 0 && L.K <= pl->fold_max_k && pl->identity &&
                S.split[li] == 1) {   // split-K adds the residual in its finalize pass
       if (!make_tmap_bf16(&S.tmR[li], S.act[res_t], (uint64_t)M, (uint64_t)N, (uint64_t)N * 2,
@@ -1600,7 +1582,6 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* fb = knob("B2_FORCE_BN")) pl->force_bn = atoi(fb);
   if (const char* pd = knob("B2_PDL")) g_pdl = pd[0] != '0';
   if (const char* fk = knob("B2_FOLD_MAX_K")) pl->fold_max_k = atoi(fk);
-  if (const char* rt = knob("B2_RES_TMA")) pl->use_res_tma = rt[0] != '0';
   if (const char* ic = knob("B2_IM2COL")) pl->use_im2col = ic[0] != '0';
   if (const char* i8 = knob("B2_IM2COL8")) pl->im2col8 = i8[0] == '1';
   if (const char* sd = knob("B2_S2D")) pl->use_s2d = sd[0] != '0';

@@ -22,7 +22,7 @@ constexpr long ROWS = BYTES / (ROW_ELEMS * 2);
 
 // Each CTA walks boxes b = blockIdx.x, += gridDim.x; box b covers rows
 // (b / nbx) * box_rows.., columns (b % nbx) * box_cols.
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(256, 1)
     tma_store_kernel(const __grid_constant__ CUtensorMap m, int box_rows, int box_cols, int depth,
                      const __grid_constant__ CUtensorMap src, int mix) {
   extern __shared__ uint8_t raw[];
@@ -37,12 +37,17 @@ __global__ void __launch_bounds__(128, 1)
   }
   fence_proxy_async_smem();
   __syncthreads();
-  if (threadIdx.x != 0) return;
+  // `mix` > 1: that many issuing warps (lane 0 each), boxes interleaved
+  const int issuers = mix > 1 ? mix : 1;
+  const int wi = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) != 0 || wi >= issuers) return;
+  if (mix > 1) mix = 0;
+  sm += wi * depth * box_bytes;
   const long nbx = ROW_ELEMS / box_cols;
   const long nbox = (ROWS / box_rows) * nbx;
   int k = 0;
   uint32_t ph = 0;
-  for (long b = blockIdx.x; b < nbox; b += gridDim.x, ++k) {
+  for (long b = (long)blockIdx.x * issuers + wi; b < nbox; b += (long)gridDim.x * issuers, ++k) {
     const int slot = k % depth;
     const int c0 = (int)(b % nbx) * box_cols, r0 = (int)(b / nbx) * box_rows;
     if (mix) {   // read one box (from the other half of the buffer) into the slot first
@@ -53,6 +58,7 @@ __global__ void __launch_bounds__(128, 1)
       ph ^= 1;
     } else if (k >= depth) {   // throttle: at most `depth` stores in flight
       switch (depth) {
+        case 2: bulk_wait_read<1>(); break;
         case 4: bulk_wait_read<3>(); break;
         case 8: bulk_wait_read<7>(); break;
         case 16: bulk_wait_read<15>(); break;
@@ -109,7 +115,10 @@ int main() {
   struct Shape { int rows, cols; CUtensorMapSwizzle sw; const char* name; };
   Shape shapes[] = {{32, 32, CU_TENSOR_MAP_SWIZZLE_64B, "32 rows x 64 B (gemm epilogue)"},
                     {32, 64, CU_TENSOR_MAP_SWIZZLE_128B, "32 rows x 128 B"},
+                    {128, 32, CU_TENSOR_MAP_SWIZZLE_64B, "128 rows x 64 B"},
+                    {64, 64, CU_TENSOR_MAP_SWIZZLE_128B, "64 rows x 128 B"},
                     {128, 64, CU_TENSOR_MAP_SWIZZLE_128B, "128 rows x 128 B (chain)"},
+                    {256, 64, CU_TENSOR_MAP_SWIZZLE_128B, "256 rows x 128 B"},
                     {64, 256, CU_TENSOR_MAP_SWIZZLE_NONE, "64 rows x 512 B (no swizzle)"}};
   for (auto& s : shapes) {
     CUtensorMap m, ms;
@@ -130,6 +139,13 @@ int main() {
         tma_store_kernel<<<sms, 128, depth * bb + 1024>>>(m, s.rows, s.cols, depth, ms, 0);
       });
       printf("TMA store  %-32s depth %2d: %6.2f TB/s\n", s.name, depth, BYTES / ms_ / 1e9);
+    }
+    for (int iss : {2, 4, 8}) {   // several issuing warps per SM, depth 2 each
+      if (iss * 2 * bb > 190 * 1024) continue;
+      const float ms_ = timeit([&] {
+        tma_store_kernel<<<sms, 256, iss * 2 * bb + 1024>>>(m, s.rows, s.cols, 2, ms, iss);
+      });
+      printf("TMA store  %-32s %d issuers x depth 2: %6.2f TB/s\n", s.name, iss, BYTES / ms_ / 1e9);
     }
   }
   for (int bpsm : {4, 8, 16}) {
