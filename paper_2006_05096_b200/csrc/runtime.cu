@@ -1477,6 +1477,11 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
     CK(dmalloc(pl, (void**)&S.ws, ws_elems * sizeof(float) + 256));
     CK(cudaMemset(S.ws, 0, ws_elems * sizeof(float) + 256));
   }
+  // The memsets above run on the legacy default stream, which does not order
+  // against the plan's non-blocking stream: without this the first forward at
+  // a new batch size raced the zeroing of its own activation arena (seen as
+  // wrong early rows on the first predict at b=256, right on the second).
+  CK(cudaDeviceSynchronize());
   auto res = pl->states.emplace(batch, std::move(S));
   *out = &res.first->second;
   return B2_OK;
@@ -1498,6 +1503,7 @@ int graph_of(b2_plan* pl, BatchState& S, cudaGraphExec_t* out, bool second = fal
     CK(dmalloc(pl, (void**)&S.d_in2, in_bytes(pl, S.batch) + 256));
     CK(cudaMemset(S.d_in2, 0, in_bytes(pl, S.batch) + 256));
     CK(dmalloc(pl, (void**)&S.d_out2, (size_t)S.batch * pl->out_elems * 4 + 256));
+    CK(cudaDeviceSynchronize());   // legacy-stream memset vs the plan's non-blocking stream
   }
   int rc;
   cudaGraph_t g;
@@ -1653,8 +1659,10 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
             std::chrono::duration<double>(tv1 - tv0).count(),
             std::chrono::duration<double>(tv2 - tv1).count(), len);
   }
+  // uploads and their zero-fills ran on the legacy default stream: complete
+  // them before the plan's non-blocking stream can touch the weights
+  if (cudaDeviceSynchronize() != cudaSuccess && !rc) rc = fail(B2_ERR_CUDA, "weight upload failed");
   if (pl->stage) {
-    if (cudaDeviceSynchronize() != cudaSuccess && !rc) rc = fail(B2_ERR_CUDA, "weight upload failed");
     cudaFree(pl->stage);
     pl->stage = nullptr;
     pl->stage_bytes = 0;
