@@ -22,6 +22,13 @@ enum { ACT_NONE = 0, ACT_RELU = 1, ACT_RELU6 = 2, ACT_GELU = 3, ACT_TANH = 4 };
 // GELU(x) = x/2 (1 + erf(x / sqrt 2)). (libdevice erff's branches made the
 // GELU epilogue the bottleneck of the BERT FFN GEMM; A&S 7.1.26 needed two
 // MUFU ops per element.)
+// 1/x on the MUFU alone (__fdividef adds an FMUL and a range test + select:
+// 3 of the ~20 instructions per element of the GELU epilogue)
+B2_DEV float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 B2_DEV float gelu_erf(float v) {
   // erf by Abramowitz & Stegun 7.1.28: 1 - (1 + a1 z + ... + a6 z^6)^-16,
   // |error| <= 3e-7 (GELU within 1.1e-6 of the exact erf form over [-12, 12],
@@ -32,7 +39,7 @@ B2_DEV float gelu_erf(float v) {
   const float p = fmaf(z, fmaf(z, fmaf(z, fmaf(z, fmaf(z, fmaf(z, 0.0000430638f, 0.0002765672f),
                                                        0.0001520143f), 0.0092705272f),
                                          0.0422820123f), 0.0705230784f), 1.f);
-  float r = __fdividef(1.f, p);
+  float r = rcp_approx(p);
   r *= r;
   r *= r;
   r *= r;
@@ -73,7 +80,7 @@ B2_DEV void gelu_erf2(float& va, float& vb) {
   p = f2fma(z, p, f2pack(1.f, 1.f));
   float pa, pb;
   f2unpack(p, pa, pb);
-  uint64_t r = f2pack(__fdividef(1.f, pa), __fdividef(1.f, pb));
+  uint64_t r = f2pack(rcp_approx(pa), rcp_approx(pb));
   r = f2mul(r, r);
   r = f2mul(r, r);
   r = f2mul(r, r);
@@ -442,8 +449,13 @@ B2_DEV uint32_t mapa_shared(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+// Relaxed: the only cross-CTA arrivals are accumulator releases issued after
+// tcgen05.wait::ld, so there is nothing for a release to order — and
+// .release.cluster compiles to MEMBAR.ALL.GPU + ERRBAR before the arrive
+// (ncu: ~7% of the stall samples of the BERT FFN-up GEMM, every tile, every
+// epilogue warp of the peer CTA).
 B2_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
 // TMA loads whose completion is signalled on the pair leader's mbarrier

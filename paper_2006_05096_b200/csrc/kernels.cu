@@ -870,6 +870,105 @@ __global__ void __launch_bounds__(256) layernorm_vec_kernel(const bf16* __restri
   }
 }
 
+// bf16 LayerNorm without a residual (BERT: the residual is added by the
+// producing GEMM's epilogue), D = VPL * 256.  ncu on the one-row-per-warp
+// kernel above: 15.3 us per BERT LayerNorm at b=128, issue-bound (IPC 1.74,
+// ~17 instructions per element: gamma/beta reloaded for every row, scalar
+// fp32 math) at 50% occupancy.  Here a warp keeps its lane's gamma/beta as
+// f32x2 pairs in registers and walks rows r, r + nwarps, ... with the next
+// row's 48 bytes per lane prefetched; sums, centring, scaling and the affine
+// run on packed fma/mul/add.rn.f32x2 (FFMA2 ...): ~5 instructions per element.
+B2_DEV uint64_t f2add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+B2_DEV uint64_t bf16x2_to_f2(uint32_t w) {   // (lo, hi) bf16 pair -> (f32, f32)
+  return f2pack(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(256, 2) layernorm_rows_kernel(const bf16* __restrict__ x,
+                                                                const float* __restrict__ g,
+                                                                const float* __restrict__ bt,
+                                                                bf16* __restrict__ y, long rows,
+                                                                int D, float eps) {
+  const int lane = threadIdx.x & 31;
+  const long w0 = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long nw = (long)gridDim.x * (blockDim.x >> 5);
+  if (w0 >= rows) return;
+  uint64_t gg[VPL][4], bb[VPL][4];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const float4* gp = reinterpret_cast<const float4*>(g + (lane + 32 * i) * 8);
+    const float4* bp = reinterpret_cast<const float4*>(bt + (lane + 32 * i) * 8);
+    const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1), b0 = __ldg(bp), b1 = __ldg(bp + 1);
+    gg[i][0] = f2pack(g0.x, g0.y);
+    gg[i][1] = f2pack(g0.z, g0.w);
+    gg[i][2] = f2pack(g1.x, g1.y);
+    gg[i][3] = f2pack(g1.z, g1.w);
+    bb[i][0] = f2pack(b0.x, b0.y);
+    bb[i][1] = f2pack(b0.z, b0.w);
+    bb[i][2] = f2pack(b1.x, b1.y);
+    bb[i][3] = f2pack(b1.z, b1.w);
+  }
+  const float inv_d = 1.f / (float)D;
+  uint4 cur[VPL];
+  {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + w0 * D);
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) cur[i] = __ldg(xr + lane + 32 * i);
+  }
+  for (long r = w0; r < rows; r += nw) {
+    uint4 nxt[VPL];
+    if (r + nw < rows) {
+      const uint4* xr = reinterpret_cast<const uint4*>(x + (r + nw) * D);
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) nxt[i] = __ldg(xr + lane + 32 * i);
+    }
+    uint64_t v[VPL][4];
+    uint64_t s2 = 0;   // (+0.f, +0.f)
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      v[i][0] = bf16x2_to_f2(cur[i].x);
+      v[i][1] = bf16x2_to_f2(cur[i].y);
+      v[i][2] = bf16x2_to_f2(cur[i].z);
+      v[i][3] = bf16x2_to_f2(cur[i].w);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) s2 = f2add(s2, v[i][h]);
+    }
+    float sa, sb;
+    f2unpack(s2, sa, sb);
+    const float mean = warp_sum(sa + sb) * inv_d;
+    const uint64_t nm = f2pack(-mean, -mean);
+    uint64_t q2 = 0;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        v[i][h] = f2add(v[i][h], nm);          // centred
+        q2 = f2fma(v[i][h], v[i][h], q2);
+      }
+    f2unpack(q2, sa, sb);
+    const float rstd = rsqrtf(warp_sum(sa + sb) * inv_d + eps);
+    const uint64_t rs = f2pack(rstd, rstd);
+    uint4* yr = reinterpret_cast<uint4*>(y + r * D);
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      uint32_t o[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        float oa, ob;
+        f2unpack(f2fma(f2mul(v[i][h], rs), gg[i][h], bb[i][h]), oa, ob);
+        o[h] = pack_bf16x2(oa, ob);
+      }
+      yr[lane + 32 * i] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) cur[i] = nxt[i];
+  }
+}
+
 template <typename T>
 cudaError_t layernorm(const T* x, const T* res, const float* g, const float* b, T* y, long rows,
                       int D, float eps, cudaStream_t st) {
@@ -879,6 +978,19 @@ cudaError_t layernorm(const T* x, const T* res, const float* g, const float* b, 
       switch (D / 256) {
 #define B2_LNV(V)                                                                           \
   case V:                                                                                   \
+    if (!res) {                                                                             \
+      static int sms = 0;                                                                   \
+      if (!sms) {                                                                           \
+        int dev = 0;                                                                        \
+        cudaGetDevice(&dev);                                                                \
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                  \
+      }                                                                                     \
+      const long blocks = (rows + 7) / 8;                                                   \
+      layernorm_rows_kernel<V><<<(unsigned)(blocks < 2 * sms ? blocks : 2 * sms), 256, 0,   \
+                                 st>>>(reinterpret_cast<const bf16*>(x), g, b,              \
+                                       reinterpret_cast<bf16*>(y), rows, D, eps);           \
+      return cudaGetLastError();                                                            \
+    }                                                                                       \
     layernorm_vec_kernel<V><<<nblk(rows, 8), 256, 0, st>>>(                                 \
         reinterpret_cast<const bf16*>(x), reinterpret_cast<const bf16*>(res), g, b,         \
         reinterpret_cast<bf16*>(y), rows, D, eps);                                          \
@@ -1179,6 +1291,125 @@ cudaError_t flush_l2(void* buf, size_t bytes, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ fused 2-layer MLP
+// The reference's toy MLP (784 -> 256 -> act -> 10, BASELINE configs[0]) at
+// batch 1..64 is launch-bound: input pack + two GEMMs + output gather were
+// ~22 us per batch of graph replay for ~1 MB of weights.  One kernel instead:
+// CTA (j, g) computes hidden units [16 j, 16 j + 16) for input rows
+// [16 g, 16 g + 16) from its W1 slice and the rows staged in shared memory
+// (input rounded to the plan's storage type, exactly like the packing op); the
+// last CTA of a row group (arrival counter, reset by that CTA) computes the
+// second layer for the group's rows in a fixed order and writes the logits
+// tensor and the fp32 output.  Deterministic (every sum has one owner and one
+// order).  fp32 plans keep their weights as the 3xTF32 hi + lo split, whose
+// sum is the fp32 weight exactly.
+constexpr int MLP_NB = 16, MLP_RB = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(256) mlp2_kernel(const MlpArgs a) {
+  extern __shared__ float msm[];
+  const int K1 = a.K1, N1 = a.N1, N2 = a.N2;
+  const int ldk = K1 + 1;                       // padded rows: 16 units hit distinct banks
+  float* sw = msm;                              // [16][ldk] W1 slice
+  float* sx = msm + MLP_NB * ldk;               // [16][K1] input rows
+  __shared__ int last;
+  const int n0 = blockIdx.x * MLP_NB, r0 = blockIdx.y * MLP_RB;
+  const int rows = min(MLP_RB, a.B - r0);
+  const T* w1 = static_cast<const T*>(a.w1);
+  const T* w1l = static_cast<const T*>(a.w1lo);
+  for (int n = threadIdx.x >> 5; n < MLP_NB; n += 8)          // warp per unit row
+    for (int k = threadIdx.x & 31; k < K1; k += 32) {
+      float w = 0.f;
+      if (n0 + n < N1) {
+        w = to_f(w1[(size_t)(n0 + n) * a.ldw1 + k]);
+        if (w1l) w += to_f(w1l[(size_t)(n0 + n) * a.ldw1 + k]);
+      }
+      sw[n * ldk + k] = w;
+    }
+  for (int r = threadIdx.x >> 5; r < rows; r += 8)
+    for (int k = threadIdx.x & 31; k < K1; k += 32) {
+      const T xv = from_f<T>(a.in[(size_t)(r0 + r) * K1 + k]);
+      sx[r * K1 + k] = to_f(xv);
+      if (blockIdx.x == 0) static_cast<T*>(a.xin)[(size_t)(r0 + r) * K1 + k] = xv;
+    }
+  __syncthreads();
+  // layer 1: thread = (unit n, K lane kl); 16 lanes split each dot, shuffle-reduced
+  {
+    const int n = threadIdx.x >> 4, kl = threadIdx.x & 15;
+    const float* wr = sw + n * ldk;
+    for (int r = 0; r < rows; ++r) {
+      const float* xr = sx + r * K1;
+      float acc = 0.f;
+      for (int k = kl; k < K1; k += 16) acc = fmaf(xr[k], wr[k], acc);
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (kl == 0 && n0 + n < N1) {
+        if (a.b1) acc += a.b1[n0 + n];
+        static_cast<T*>(a.h)[(size_t)(r0 + r) * N1 + n0 + n] = from_f<T>(act_apply(acc, a.act1));
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(a.counters + blockIdx.y, 1u);
+    last = prev == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // layer 2 for this row group, by the last CTA to finish: h rows and W2 -> smem
+  float* sh = msm;                              // [rows][N1]
+  float* sw2 = msm + MLP_RB * N1;               // [N2][N1]
+  const T* hp = static_cast<const T*>(a.h);
+  for (int i = threadIdx.x; i < rows * N1; i += blockDim.x) {
+    const int rr = i / N1, k = i - rr * N1;
+    sh[i] = to_f(__ldcg(hp + (size_t)(r0 + rr) * N1 + k));
+  }
+  const T* w2 = static_cast<const T*>(a.w2);
+  const T* w2l = static_cast<const T*>(a.w2lo);
+  for (int i = threadIdx.x; i < N2 * N1; i += blockDim.x) {
+    const int m = i / N1, k = i - m * N1;
+    float w = to_f(w2[(size_t)m * a.ldw2 + k]);
+    if (w2l) w += to_f(w2l[(size_t)m * a.ldw2 + k]);
+    sw2[i] = w;
+  }
+  __syncthreads();
+  // warp per output, lanes split the N1-long dot
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int o = warp; o < rows * N2; o += 8) {
+    const int rr = o / N2, m = o - rr * N2;
+    const float* hr = sh + rr * N1;
+    const float* wr = sw2 + m * N1;
+    float acc = 0.f;
+    for (int k = lane; k < N1; k += 32) acc = fmaf(hr[k], wr[k], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      if (a.b2) acc += a.b2[m];
+      const T yv = from_f<T>(act_apply(acc, a.act2));
+      static_cast<T*>(a.y)[(size_t)(r0 + rr) * N2 + m] = yv;
+      a.out[(size_t)(r0 + rr) * a.out_stride + a.out_off + m] = to_f(yv);
+    }
+  }
+  if (threadIdx.x == 0) a.counters[blockIdx.y] = 0;   // ready for the next launch
+}
+
+template <typename T>
+cudaError_t mlp2(const MlpArgs& a, cudaStream_t st) {
+  const size_t l1 = (size_t)MLP_NB * (a.K1 + 1) + (size_t)MLP_RB * a.K1;
+  const size_t l2 = (size_t)MLP_RB * a.N1 + (size_t)a.N2 * a.N1;
+  const size_t smem = (l1 > l2 ? l1 : l2) * sizeof(float);
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(mlp2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cfg = true;
+  }
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  dim3 grid((a.N1 + MLP_NB - 1) / MLP_NB, (a.B + MLP_RB - 1) / MLP_RB);
+  mlp2_kernel<T><<<grid, 256, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ instantiations
 #define B2_INST(T)                                                                            \
   template cudaError_t gemm_simt<T>(const GemmSimtArgs&, cudaStream_t);                       \
@@ -1196,7 +1427,8 @@ cudaError_t flush_l2(void* buf, size_t bytes, cudaStream_t st) {
                                     cudaStream_t);           \
   template cudaError_t act_ew<T>(const T*, T*, long, int, cudaStream_t);                       \
   template cudaError_t output_gather<T>(const T*, float*, int, long, long, long, cudaStream_t); \
-  template cudaError_t convert_f32<T>(const float*, T*, long, cudaStream_t);
+  template cudaError_t convert_f32<T>(const float*, T*, long, cudaStream_t);                  \
+  template cudaError_t mlp2<T>(const MlpArgs&, cudaStream_t);
 B2_INST(float)
 B2_INST(bf16)
 #undef B2_INST

@@ -137,6 +137,26 @@ struct GemmSimtArgs {
   int H, W, C, OW, OHW, S, stride, pad;
 };
 
+// fused INPUT -> LINEAR(act) -> LINEAR(act) -> OUTPUT for small MLPs (kernels.cu)
+struct MlpArgs {
+  const float* in;              // fp32 input [B][K1]
+  const void* w1; const void* w1lo;   // [N1][ldw1] (T); lo part of a 3xTF32 split or nullptr
+  int ldw1;
+  const float* b1;
+  int act1;
+  const void* w2; const void* w2lo;
+  int ldw2;
+  const float* b2;
+  int act2;
+  void* xin;                    // input tensor [B][K1] (T): the packed input, for read-back
+  void* h;                      // hidden tensor [B][N1] (T)
+  void* y;                      // logits tensor [B][N2] (T)
+  float* out;                   // plan output [B][out_stride], this tensor at out_off
+  long out_stride, out_off;
+  int B, K1, N1, N2;
+  unsigned* counters;           // per 16-row group, zero between launches
+};
+template <typename T> cudaError_t mlp2(const MlpArgs& a, cudaStream_t st);
 template <typename T> cudaError_t gemm_simt(const GemmSimtArgs& a, cudaStream_t st);
 template <typename T>
 cudaError_t input_pack(const float* in, T* out, int B, int C, int H, int W, int Cp,

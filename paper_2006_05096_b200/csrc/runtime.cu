@@ -266,6 +266,7 @@ struct BatchState {
   std::vector<CUtensorMap> tmO;    // per layer (tc): output, 32x32 box, 64B swizzle
   std::vector<CUtensorMap> tmR;    // per layer (tc, residual fold): residual as an A operand
   std::vector<char> fold;          // per layer: residual folded into the MMA
+  unsigned* mlp_ctr = nullptr;     // fused MLP: per-16-row-group arrival counters
   std::vector<char> a_narrow;      // per layer: A box width for K <= 32 (0 = 64)
   std::vector<CUtensorMap> tmI;    // per layer: identity [256 x 256] (box rows = BN) for the fold
   std::vector<char> band;          // per layer: banded implicit-GEMM conv (conv_band.cu)
@@ -328,6 +329,8 @@ struct b2_plan {
   bool alt_order = true;         // B2_ALT_ORDER=0 -> every GEMM walks M tiles forward
   bool use_split = true;         // B2_SPLIT=0 -> no split-K at small batch
   bool use_chain = true;         // B2_CHAIN=0 -> block-tail and next conv1 as two GEMMs
+  bool use_mlp_fusion = true;    // B2_MLP_FUSE=0 -> the toy MLP as pack + 2 GEMMs + gather
+  int mlp_in = -1, mlp_l1 = -1, mlp_l2 = -1, mlp_out = -1;   // fused 2-layer MLP (plan_fuse_mlp)
   int band_max_n = 128;      // B2_BAND_MAX_N: widest conv (output channels) sent to conv_band
   void* identity = nullptr;  // bf16 I[256][256]
   void* stage = nullptr;     // weight-upload staging (plan creation only)
@@ -828,6 +831,38 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
       nvtxRangePushA(nm);
       CK(cudaEventRecord(op_events[li], st));
     }
+    if (pl->mlp_in >= 0) {      // fused 2-layer MLP: one launch at the input op
+      if ((int)li == pl->mlp_in) {
+        const Layer &A = pl->layers[pl->mlp_l1], &Bl = pl->layers[pl->mlp_l2];
+        MlpArgs m{};
+        m.in = static_cast<const float*>(d_in);
+        m.w1 = A.w;
+        m.w1lo = A.tf32 ? A.w2 : nullptr;
+        m.ldw1 = A.ldw;
+        m.b1 = A.bias;
+        m.act1 = A.p[7];
+        m.w2 = Bl.w;
+        m.w2lo = Bl.tf32 ? Bl.w2 : nullptr;
+        m.ldw2 = Bl.ldw;
+        m.b2 = Bl.bias;
+        m.act2 = Bl.p[7];
+        m.xin = S.act[p[0]];
+        m.h = S.act[A.p[1]];
+        m.y = S.act[Bl.p[1]];
+        m.out = d_out;
+        m.out_stride = (long)pl->out_elems;
+        m.out_off = 0;
+        m.B = B;
+        m.K1 = A.p[4];
+        m.N1 = A.p[5];
+        m.N2 = Bl.p[5];
+        m.counters = S.mlp_ctr;
+        CK(mlp2<T>(m, st));
+        ++launches;
+        continue;
+      }
+      if ((int)li == pl->mlp_l1 || (int)li == pl->mlp_l2 || (int)li == pl->mlp_out) continue;
+    }
     switch (L.kind) {
       case OP_INPUT:
         if (L.s2d)
@@ -1300,6 +1335,11 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
   for (size_t t = 0; t < pl->tensors.size(); ++t) S.act[t] = static_cast<uint8_t*>(S.arena) + off[t];
   CK(dmalloc(pl, (void**)&S.d_in, in_bytes(pl, batch) + 256));
   CK(cudaMemset(S.d_in, 0, in_bytes(pl, batch) + 256));
+  if (pl->mlp_in >= 0) {
+    const size_t groups = (size_t)(batch + 15) / 16;
+    CK(dmalloc(pl, (void**)&S.mlp_ctr, groups * sizeof(unsigned) + 256));
+    CK(cudaMemset(S.mlp_ctr, 0, groups * sizeof(unsigned) + 256));
+  }
   CK(dmalloc(pl, (void**)&S.d_out, (size_t)batch * pl->out_elems * 4 + 256));
   S.bn.assign(pl->layers.size(), 0);
   S.tmA.resize(pl->layers.size());
@@ -1545,6 +1585,28 @@ const char* b2_last_error(void) { return g_err.c_str(); }
 
 const char* b2_version(void) { return "libb2 0.1 sm_100a (tcgen05/TMA bf16, SIMT fp32)"; }
 
+// INPUT (flat, unpadded) -> LINEAR -> LINEAR -> OUTPUT (only that tensor) with
+// the hidden tensor consumed by the second linear alone: one mlp2 launch.
+void plan_fuse_mlp(b2_plan* pl) {
+  if (!pl->use_mlp_fusion || pl->force_simt || pl->layers.size() != 4) return;
+  const Layer &I = pl->layers[0], &A = pl->layers[1], &Bl = pl->layers[2], &O = pl->layers[3];
+  if (I.kind != OP_INPUT || A.kind != OP_LINEAR || Bl.kind != OP_LINEAR || O.kind != OP_OUTPUT)
+    return;
+  const int *pi = I.p, *pa = A.p, *pb = Bl.p, *po = O.p;
+  if (pi[2] != 1 || pi[3] != 1 || pi[4] != pi[1]) return;             // flat input, no padding
+  if (pa[0] != pi[0] || pa[6] != 1 || pa[8] >= 0 || pa[9] != pa[4]) return;
+  if (pb[0] != pa[1] || pb[6] != 1 || pb[8] >= 0 || pb[9] != pb[4]) return;
+  if (po[0] != 1 || po[1] != pb[1] || po[2] != 0) return;
+  if (pa[4] != pi[1] || pb[4] != pa[5] || pa[4] > 2048 || pb[5] > 256 || pa[5] > 1024) return;
+  const size_t l1 = (size_t)16 * (pa[4] + 1) + (size_t)16 * pa[4];
+  const size_t l2 = (size_t)16 * pa[5] + (size_t)pb[5] * pa[5];
+  if ((l1 > l2 ? l1 : l2) * sizeof(float) > 200 * 1024) return;      // shared-memory staging
+  pl->mlp_in = 0;
+  pl->mlp_l1 = 1;
+  pl->mlp_l2 = 2;
+  pl->mlp_out = 3;
+}
+
 int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (!blob || !out) return fail(B2_ERR_ARG, "null argument");
   *out = nullptr;
@@ -1604,6 +1666,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* ao = knob("B2_ALT_ORDER")) pl->alt_order = ao[0] != '0';
   if (const char* sk = knob("B2_SPLIT")) pl->use_split = sk[0] != '0';
   if (const char* cz = knob("B2_CHAIN")) pl->use_chain = cz[0] != '0';
+  if (const char* mf = knob("B2_MLP_FUSE")) pl->use_mlp_fusion = mf[0] != '0';
   if (const char* bm = knob("B2_BAND_MAX_N")) pl->band_max_n = atoi(bm);
   const auto tv0 = std::chrono::steady_clock::now();
   cudaFree(nullptr);   // context creation, timed separately under B2_VERBOSE
@@ -1642,6 +1705,7 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (!rc) plan_fuse_pool(pl);
   if (!rc) plan_fold_downsample(pl);
   if (!rc) plan_chain(pl);
+  if (!rc) plan_fuse_mlp(pl);
   if (!rc) rc = upload_weights(pl, d + pos, wr, len - 4 - pos);
   if (!rc && pl->dtype == B2_DT_BF16) {
     std::vector<float> eye(256 * 256, 0.f);
@@ -1959,6 +2023,7 @@ void b2_plan_destroy(b2_plan* pl) {
     if (S.h_out) cudaFreeHost(S.h_out);
     if (S.graph2) cudaGraphExecDestroy(S.graph2);
     if (S.ws) cudaFree(S.ws);
+    if (S.mlp_ctr) cudaFree(S.mlp_ctr);
     if (S.d_in2) cudaFree(S.d_in2);
     if (S.d_out2) cudaFree(S.d_out2);
     if (S.h_out2) cudaFreeHost(S.h_out2);

@@ -1,0 +1,14 @@
+cd $GRAFT_REPO_ROOT
+for m in "mlp 1" "mlp 64" "mlp 256"; do
+  AB_LABEL=new timeout 300 python tools/fwd_time.py $m >> gpurun_out/ab.txt 2>&1
+  B2_LIB=ab/libb2_base.so AB_LABEL=base timeout 300 python tools/fwd_time.py $m >> gpurun_out/ab.txt 2>&1
+done
+for rep in 1 2; do
+for m in "bert 128" "resnet50 256"; do
+  AB_LABEL=new timeout 300 python tools/fwd_time.py $m >> gpurun_out/ab.txt 2>&1
+  B2_LIB=ab/libb2_base.so AB_LABEL=base timeout 300 python tools/fwd_time.py $m >> gpurun_out/ab.txt 2>&1
+done
+done
+sort -k2,3 -s gpurun_out/ab.txt
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 2400 python -m pytest tests/test_gpu.py tests/test_gpu_fullsize.py tests/test_gpu_bert_mask.py -q -rf 2>&1 | tail -4
