@@ -913,6 +913,10 @@ __global__ void __launch_bounds__(256, 2) layernorm_rows_kernel(const bf16* __re
     bb[i][3] = f2pack(b1.z, b1.w);
   }
   const float inv_d = 1.f / (float)D;
+  // PDL: launched while the producing GEMM drains; gamma/beta (weights) are
+  // read before the wait, the rows after it
+  pdl_wait();
+  pdl_launch_dependents();
   uint4 cur[VPL];
   {
     const uint4* xr = reinterpret_cast<const uint4*>(x + w0 * D);
@@ -986,10 +990,10 @@ cudaError_t layernorm(const T* x, const T* res, const float* g, const float* b, 
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                  \
       }                                                                                     \
       const long blocks = (rows + 7) / 8;                                                   \
-      layernorm_rows_kernel<V><<<(unsigned)(blocks < 2 * sms ? blocks : 2 * sms), 256, 0,   \
-                                 st>>>(reinterpret_cast<const bf16*>(x), g, b,              \
-                                       reinterpret_cast<bf16*>(y), rows, D, eps);           \
-      return cudaGetLastError();                                                            \
+      return launch_pdl(layernorm_rows_kernel<V>,                                           \
+                        dim3((unsigned)(blocks < 2 * sms ? blocks : 2 * sms)), dim3(256), 0, st, \
+                        reinterpret_cast<const bf16*>(x), g, b, reinterpret_cast<bf16*>(y),  \
+                        rows, D, eps);                                                      \
     }                                                                                       \
     layernorm_vec_kernel<V><<<nblk(rows, 8), 256, 0, st>>>(                                 \
         reinterpret_cast<const bf16*>(x), reinterpret_cast<const bf16*>(res), g, b,         \
@@ -1305,46 +1309,76 @@ cudaError_t flush_l2(void* buf, size_t bytes, cudaStream_t st) {
 // sum is the fp32 weight exactly.
 constexpr int MLP_NB = 16, MLP_RB = 16;
 
+// Rows [nrows][bytes] at a source pitch into shared memory at a destination
+// pitch with one bulk copy per row, all in flight at once on one mbarrier
+// (a tiny MLP is latency-bound: element-wise staging loops cost one L2/DRAM
+// round trip per few elements — 73 us for a 2 MB problem in the first version).
+B2_DEV void bulk_rows(void* dst, uint32_t dst_pitch, const void* src, size_t src_pitch, int nrows,
+                      uint32_t bytes, uint64_t* bar) {
+  for (int r = 0; r < nrows; ++r)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(static_cast<uint8_t*>(dst) + (size_t)r * dst_pitch)),
+        "l"(static_cast<const uint8_t*>(src) + (size_t)r * src_pitch), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) mlp2_kernel(const MlpArgs a) {
-  extern __shared__ float msm[];
+  extern __shared__ __align__(16) uint8_t mraw[];
   const int K1 = a.K1, N1 = a.N1, N2 = a.N2;
-  const int ldk = K1 + 1;                       // padded rows: 16 units hit distinct banks
-  float* sw = msm;                              // [16][ldk] W1 slice
-  float* sx = msm + MLP_NB * ldk;               // [16][K1] input rows
+  const bool split = a.w1lo != nullptr;              // fp32 plan: 3xTF32 hi + lo weights
+  const uint32_t k1b = (uint32_t)K1 * sizeof(T), k1p = (k1b + 15) & ~15u;
+  T* sw = reinterpret_cast<T*>(mraw);                // [16][k1p bytes] W1 slice (hi)
+  T* swl = reinterpret_cast<T*>(mraw + MLP_NB * k1p);   // lo part (fp32 plans)
+  float* sx = reinterpret_cast<float*>(mraw + (split ? 2 : 1) * MLP_NB * k1p);   // [16][K1]
+  __shared__ uint64_t bar;
   __shared__ int last;
+  __shared__ float sb2[256];
   const int n0 = blockIdx.x * MLP_NB, r0 = blockIdx.y * MLP_RB;
-  const int rows = min(MLP_RB, a.B - r0);
-  const T* w1 = static_cast<const T*>(a.w1);
-  const T* w1l = static_cast<const T*>(a.w1lo);
-  for (int n = threadIdx.x >> 5; n < MLP_NB; n += 8)          // warp per unit row
-    for (int k = threadIdx.x & 31; k < K1; k += 32) {
-      float w = 0.f;
-      if (n0 + n < N1) {
-        w = to_f(w1[(size_t)(n0 + n) * a.ldw1 + k]);
-        if (w1l) w += to_f(w1l[(size_t)(n0 + n) * a.ldw1 + k]);
-      }
-      sw[n * ldk + k] = w;
-    }
-  for (int r = threadIdx.x >> 5; r < rows; r += 8)
-    for (int k = threadIdx.x & 31; k < K1; k += 32) {
-      const T xv = from_f<T>(a.in[(size_t)(r0 + r) * K1 + k]);
-      sx[r * K1 + k] = to_f(xv);
-      if (blockIdx.x == 0) static_cast<T*>(a.xin)[(size_t)(r0 + r) * K1 + k] = xv;
-    }
+  const int rows = min(MLP_RB, a.B - r0), units = min(MLP_NB, N1 - n0);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&bar, (uint32_t)(units * k1b * (split ? 2 : 1) + rows * K1 * 4));
+    const size_t wp = (size_t)a.ldw1 * sizeof(T);
+    bulk_rows(sw, k1p, static_cast<const T*>(a.w1) + (size_t)n0 * a.ldw1, wp, units, k1b, &bar);
+    if (split)
+      bulk_rows(swl, k1p, static_cast<const T*>(a.w1lo) + (size_t)n0 * a.ldw1, wp, units, k1b, &bar);
+    bulk_rows(sx, K1 * 4, a.in + (size_t)r0 * K1, (size_t)K1 * 4, rows, K1 * 4, &bar);
+  }
+  mbar_wait(&bar, 0);
+  // input rounded through the plan's storage type, like the packing op it replaces
+  for (int e = threadIdx.x; e < rows * K1; e += blockDim.x) {
+    const T xt = from_f<T>(sx[e]);
+    sx[e] = to_f(xt);
+    if (blockIdx.x == 0) static_cast<T*>(a.xin)[(size_t)r0 * K1 + e] = xt;
+  }
   __syncthreads();
   // layer 1: thread = (unit n, K lane kl); 16 lanes split each dot, shuffle-reduced
   {
     const int n = threadIdx.x >> 4, kl = threadIdx.x & 15;
-    const float* wr = sw + n * ldk;
+    const T* wr = reinterpret_cast<const T*>(reinterpret_cast<const uint8_t*>(sw) + n * k1p);
+    const T* wl = reinterpret_cast<const T*>(reinterpret_cast<const uint8_t*>(swl) + n * k1p);
+    const float bias1 = (a.b1 && n < units) ? __ldg(a.b1 + n0 + n) : 0.f;   // hoisted: an L2
+    // round trip per row on the critical path cost more than the dots
     for (int r = 0; r < rows; ++r) {
       const float* xr = sx + r * K1;
       float acc = 0.f;
-      for (int k = kl; k < K1; k += 16) acc = fmaf(xr[k], wr[k], acc);
+      if (n < units)
+#pragma unroll 7
+        for (int k = kl; k < K1; k += 16) {
+          float w = to_f(wr[k]);
+          if (split) w += to_f(wl[k]);
+          acc = fmaf(xr[k], w, acc);
+        }
 #pragma unroll
       for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (kl == 0 && n0 + n < N1) {
-        if (a.b1) acc += a.b1[n0 + n];
+      if (kl == 0 && n < units) {
+        acc += bias1;
         static_cast<T*>(a.h)[(size_t)(r0 + r) * N1 + n0 + n] = from_f<T>(act_apply(acc, a.act1));
       }
     }
@@ -1357,35 +1391,42 @@ __global__ void __launch_bounds__(256) mlp2_kernel(const MlpArgs a) {
   }
   __syncthreads();
   if (!last) return;
+  // layer 2 for this row group, by the last CTA to arrive: h rows (written by
+  // the other CTAs of this launch; bulk copies read through L2) and W2
   __threadfence();
-  // layer 2 for this row group, by the last CTA to finish: h rows and W2 -> smem
-  float* sh = msm;                              // [rows][N1]
-  float* sw2 = msm + MLP_RB * N1;               // [N2][N1]
-  const T* hp = static_cast<const T*>(a.h);
-  for (int i = threadIdx.x; i < rows * N1; i += blockDim.x) {
-    const int rr = i / N1, k = i - rr * N1;
-    sh[i] = to_f(__ldcg(hp + (size_t)(r0 + rr) * N1 + k));
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  const uint32_t n1b = (uint32_t)N1 * sizeof(T), n1p = (n1b + 15) & ~15u;
+  T* sh = reinterpret_cast<T*>(mraw);                                  // [rows][n1p bytes]
+  T* sw2 = reinterpret_cast<T*>(mraw + MLP_RB * n1p);                  // [N2][n1p bytes]
+  T* sw2l = reinterpret_cast<T*>(mraw + (MLP_RB + N2) * n1p);
+  const bool split2 = a.w2lo != nullptr;
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&bar, (uint32_t)(rows * n1b + N2 * n1b * (split2 ? 2 : 1)));
+    const size_t wp = (size_t)a.ldw2 * sizeof(T);
+    bulk_rows(sh, n1p, static_cast<const T*>(a.h) + (size_t)r0 * N1, n1b, rows, n1b, &bar);
+    bulk_rows(sw2, n1p, a.w2, wp, N2, n1b, &bar);
+    if (split2) bulk_rows(sw2l, n1p, a.w2lo, wp, N2, n1b, &bar);
   }
-  const T* w2 = static_cast<const T*>(a.w2);
-  const T* w2l = static_cast<const T*>(a.w2lo);
-  for (int i = threadIdx.x; i < N2 * N1; i += blockDim.x) {
-    const int m = i / N1, k = i - m * N1;
-    float w = to_f(w2[(size_t)m * a.ldw2 + k]);
-    if (w2l) w += to_f(w2l[(size_t)m * a.ldw2 + k]);
-    sw2[i] = w;
-  }
+  for (int m = threadIdx.x; m < N2; m += blockDim.x) sb2[m] = a.b2 ? __ldg(a.b2 + m) : 0.f;
+  mbar_wait(&bar, 1);
   __syncthreads();
   // warp per output, lanes split the N1-long dot
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int o = warp; o < rows * N2; o += 8) {
     const int rr = o / N2, m = o - rr * N2;
-    const float* hr = sh + rr * N1;
-    const float* wr = sw2 + m * N1;
+    const T* hr = reinterpret_cast<const T*>(reinterpret_cast<const uint8_t*>(sh) + rr * n1p);
+    const T* wr = reinterpret_cast<const T*>(reinterpret_cast<const uint8_t*>(sw2) + m * n1p);
+    const T* wl = reinterpret_cast<const T*>(reinterpret_cast<const uint8_t*>(sw2l) + m * n1p);
     float acc = 0.f;
-    for (int k = lane; k < N1; k += 32) acc = fmaf(hr[k], wr[k], acc);
+#pragma unroll 8
+    for (int k = lane; k < N1; k += 32) {
+      float w = to_f(wr[k]);
+      if (split2) w += to_f(wl[k]);
+      acc = fmaf(to_f(hr[k]), w, acc);
+    }
     acc = warp_sum(acc);
     if (lane == 0) {
-      if (a.b2) acc += a.b2[m];
+      acc += sb2[m];
       const T yv = from_f<T>(act_apply(acc, a.act2));
       static_cast<T*>(a.y)[(size_t)(r0 + rr) * N2 + m] = yv;
       a.out[(size_t)(r0 + rr) * a.out_stride + a.out_off + m] = to_f(yv);
@@ -1396,9 +1437,15 @@ __global__ void __launch_bounds__(256) mlp2_kernel(const MlpArgs a) {
 
 template <typename T>
 cudaError_t mlp2(const MlpArgs& a, cudaStream_t st) {
-  const size_t l1 = (size_t)MLP_NB * (a.K1 + 1) + (size_t)MLP_RB * a.K1;
-  const size_t l2 = (size_t)MLP_RB * a.N1 + (size_t)a.N2 * a.N1;
-  const size_t smem = (l1 > l2 ? l1 : l2) * sizeof(float);
+  const size_t k1p = ((size_t)a.K1 * sizeof(T) + 15) & ~size_t(15);
+  const size_t n1p = ((size_t)a.N1 * sizeof(T) + 15) & ~size_t(15);
+  const int sp = a.w1lo ? 2 : 1;
+  const size_t l1 = sp * MLP_NB * k1p + (size_t)MLP_RB * a.K1 * 4;
+  const size_t l2 = (MLP_RB + (size_t)a.N2 * sp) * n1p;
+  const size_t smem = l1 > l2 ? l1 : l2;
+  if ((a.K1 * sizeof(T)) % 16 || (a.N1 * sizeof(T)) % 16 || (a.ldw1 * sizeof(T)) % 16 ||
+      (a.ldw2 * sizeof(T)) % 16 || (a.K1 * 4) % 16)
+    return cudaErrorInvalidValue;   // bulk copies need 16-byte rows
   static bool cfg = false;
   if (!cfg) {
     cudaFuncSetAttribute(mlp2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

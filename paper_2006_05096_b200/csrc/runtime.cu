@@ -1598,9 +1598,10 @@ void plan_fuse_mlp(b2_plan* pl) {
   if (pb[0] != pa[1] || pb[6] != 1 || pb[8] >= 0 || pb[9] != pb[4]) return;
   if (po[0] != 1 || po[1] != pb[1] || po[2] != 0) return;
   if (pa[4] != pi[1] || pb[4] != pa[5] || pa[4] > 2048 || pb[5] > 256 || pa[5] > 1024) return;
-  const size_t l1 = (size_t)16 * (pa[4] + 1) + (size_t)16 * pa[4];
-  const size_t l2 = (size_t)16 * pa[5] + (size_t)pb[5] * pa[5];
-  if ((l1 > l2 ? l1 : l2) * sizeof(float) > 200 * 1024) return;      // shared-memory staging
+  // shared-memory staging (fp32 plans: hi + lo weight rows) and 16-byte bulk rows
+  const size_t l1 = 2 * 16 * (size_t)pa[4] * 4 + (size_t)16 * pa[4] * 4;
+  const size_t l2 = (16 + 2 * (size_t)pb[5]) * pa[5] * 4;
+  if ((l1 > l2 ? l1 : l2) > 200 * 1024 || pa[4] % 8 || pa[5] % 8) return;
   pl->mlp_in = 0;
   pl->mlp_l1 = 1;
   pl->mlp_l2 = 2;
