@@ -124,9 +124,44 @@ def cpu_baseline(model: str, plan_bytes: bytes, seconds: float = 12.0, batch: in
         el = time.perf_counter() - t0
         if el >= seconds or n >= 50:
             break
-    return {"value": n * batch / el, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-            "sample": f"{n} x {model} fp32 forwards of batch {batch} (numpy oracle, "
-                      f"{el:.1f} s)"}
+    out = {"value": n * batch / el, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+           "sample": f"{n} x {model} fp32 forwards of batch {batch} (numpy oracle, "
+                     f"{el:.1f} s)"}
+    tc = torch_cpu_forward(model, batch, seconds / 2)
+    if tc:
+        out["torch_cpu_fp32"] = tc
+    return out
+
+
+def torch_cpu_forward(model: str, batch: int, seconds: float) -> dict | None:
+    """BASELINE.md §2(ii)'s compute baseline beside the port: the torchvision /
+    transformers fp32 forward on all host threads (random init, same shapes),
+    bounded to ~`seconds`.  Supplementary: the reference itself computes
+    nothing, the oracle port above is the contract's cpu_baseline."""
+    try:
+        import torch
+        torch.set_num_threads(os.cpu_count())
+        if model == "bert":
+            from transformers import BertConfig, BertModel
+            net = BertModel(BertConfig()).eval()
+            x = torch.randint(0, 30522, (batch, 128))
+        else:
+            import torchvision
+            net = getattr(torchvision.models, model)(weights=None).eval()
+            x = torch.randn(batch, 3, 224, 224)
+        with torch.inference_mode():
+            net(x)
+            n, t0 = 0, time.perf_counter()
+            while True:
+                net(x)
+                n += 1
+                el = time.perf_counter() - t0
+                if el >= seconds or n >= 50:
+                    break
+        return {"value": round(n * batch / el, 2), "unit": UNIT, "threads": os.cpu_count(),
+                "sample": f"{n} x torch CPU fp32 {model} forwards of batch {batch} ({el:.1f} s)"}
+    except Exception as e:  # torchvision / transformers missing on the box: say so
+        return {"unavailable": f"{type(e).__name__}: {e}"[:160]}
 
 
 def roofline(plan, model: str, batch: int, ms_per_step: float, pk: dict) -> dict:

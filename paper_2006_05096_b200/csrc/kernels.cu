@@ -1307,15 +1307,27 @@ cudaError_t flush_l2(void* buf, size_t bytes, cudaStream_t st) {
 // tensor and the fp32 output.  Deterministic (every sum has one owner and one
 // order).  fp32 plans keep their weights as the 3xTF32 hi + lo split, whose
 // sum is the fp32 weight exactly.
-constexpr int MLP_NB = 16, MLP_RB = 16;
+constexpr int MLP_NB = 8, MLP_RB = 16;
+
+// four consecutive storage elements as fp32 (8-byte bf16 / 16-byte fp32 loads)
+template <typename T> B2_DEV float4 ld4f(const T* p);
+template <> B2_DEV float4 ld4f<float>(const float* p) { return *reinterpret_cast<const float4*>(p); }
+template <> B2_DEV float4 ld4f<bf16>(const bf16* p) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const float2 a = unpack_bf16x2(u.x), b = unpack_bf16x2(u.y);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
 
 // Rows [nrows][bytes] at a source pitch into shared memory at a destination
-// pitch with one bulk copy per row, all in flight at once on one mbarrier
-// (a tiny MLP is latency-bound: element-wise staging loops cost one L2/DRAM
-// round trip per few elements — 73 us for a 2 MB problem in the first version).
+// pitch, one bulk copy per row, row r issued by thread `first + r` so the
+// copies run concurrently (bulk copies issued by one thread complete one at a
+// time, ~0.3 us each: serial issue made the staging 17 us).  A tiny MLP is
+// latency-bound: the first version's element-wise staging loops paid one
+// L2/DRAM round trip per few elements (73 us for a 2 MB problem).
 B2_DEV void bulk_rows(void* dst, uint32_t dst_pitch, const void* src, size_t src_pitch, int nrows,
-                      uint32_t bytes, uint64_t* bar) {
-  for (int r = 0; r < nrows; ++r)
+                      uint32_t bytes, uint64_t* bar, int first) {
+  const int r = (int)threadIdx.x - first;
+  if (r >= 0 && r < nrows)
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
             smem_u32(static_cast<uint8_t*>(dst) + (size_t)r * dst_pitch)),
@@ -1340,15 +1352,16 @@ __global__ void __launch_bounds__(256) mlp2_kernel(const MlpArgs a) {
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_barrier_init();
+    mbar_arrive_expect_tx(&bar, (uint32_t)(units * k1b * (split ? 2 : 1) + rows * K1 * 4));
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(&bar, (uint32_t)(units * k1b * (split ? 2 : 1) + rows * K1 * 4));
+  {
     const size_t wp = (size_t)a.ldw1 * sizeof(T);
-    bulk_rows(sw, k1p, static_cast<const T*>(a.w1) + (size_t)n0 * a.ldw1, wp, units, k1b, &bar);
+    bulk_rows(sw, k1p, static_cast<const T*>(a.w1) + (size_t)n0 * a.ldw1, wp, units, k1b, &bar, 0);
     if (split)
-      bulk_rows(swl, k1p, static_cast<const T*>(a.w1lo) + (size_t)n0 * a.ldw1, wp, units, k1b, &bar);
-    bulk_rows(sx, K1 * 4, a.in + (size_t)r0 * K1, (size_t)K1 * 4, rows, K1 * 4, &bar);
+      bulk_rows(swl, k1p, static_cast<const T*>(a.w1lo) + (size_t)n0 * a.ldw1, wp, units, k1b,
+                &bar, 32);
+    bulk_rows(sx, K1 * 4, a.in + (size_t)r0 * K1, (size_t)K1 * 4, rows, K1 * 4, &bar, 64);
   }
   mbar_wait(&bar, 0);
   // input rounded through the plan's storage type, like the packing op it replaces
@@ -1358,9 +1371,11 @@ __global__ void __launch_bounds__(256) mlp2_kernel(const MlpArgs a) {
     if (blockIdx.x == 0) static_cast<T*>(a.xin)[(size_t)r0 * K1 + e] = xt;
   }
   __syncthreads();
-  // layer 1: thread = (unit n, K lane kl); 16 lanes split each dot, shuffle-reduced
+  // layer 1: warp = hidden unit, its 32 lanes split the K1-long dot in 4-wide
+  // vectors (8- / 16-byte shared loads: element-wise loads made the dots
+  // shared-memory-instruction bound), shuffle-reduced
   {
-    const int n = threadIdx.x >> 4, kl = threadIdx.x & 15;
+    const int n = threadIdx.x >> 5, kl = threadIdx.x & 31;
     const T* wr = reinterpret_cast<const T*>(reinterpret_cast<const uint8_t*>(sw) + n * k1p);
     const T* wl = reinterpret_cast<const T*>(reinterpret_cast<const uint8_t*>(swl) + n * k1p);
     const float bias1 = (a.b1 && n < units) ? __ldg(a.b1 + n0 + n) : 0.f;   // hoisted: an L2
@@ -1369,14 +1384,17 @@ __global__ void __launch_bounds__(256) mlp2_kernel(const MlpArgs a) {
       const float* xr = sx + r * K1;
       float acc = 0.f;
       if (n < units)
-#pragma unroll 7
-        for (int k = kl; k < K1; k += 16) {
-          float w = to_f(wr[k]);
-          if (split) w += to_f(wl[k]);
-          acc = fmaf(xr[k], w, acc);
+#pragma unroll 4
+        for (int k = kl * 4; k < K1; k += 128) {
+          float4 w = ld4f<T>(wr + k);
+          if (split) {
+            const float4 l = ld4f<T>(wl + k);
+            w.x += l.x; w.y += l.y; w.z += l.z; w.w += l.w;
+          }
+          const float4 x = *reinterpret_cast<const float4*>(xr + k);
+          acc = fmaf(x.x, w.x, fmaf(x.y, w.y, fmaf(x.z, w.z, fmaf(x.w, w.w, acc))));
         }
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      acc = warp_sum(acc);
       if (kl == 0 && n < units) {
         acc += bias1;
         static_cast<T*>(a.h)[(size_t)(r0 + r) * N1 + n0 + n] = from_f<T>(act_apply(acc, a.act1));
@@ -1400,12 +1418,14 @@ __global__ void __launch_bounds__(256) mlp2_kernel(const MlpArgs a) {
   T* sw2 = reinterpret_cast<T*>(mraw + MLP_RB * n1p);                  // [N2][n1p bytes]
   T* sw2l = reinterpret_cast<T*>(mraw + (MLP_RB + N2) * n1p);
   const bool split2 = a.w2lo != nullptr;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0)
     mbar_arrive_expect_tx(&bar, (uint32_t)(rows * n1b + N2 * n1b * (split2 ? 2 : 1)));
+  __syncthreads();
+  {
     const size_t wp = (size_t)a.ldw2 * sizeof(T);
-    bulk_rows(sh, n1p, static_cast<const T*>(a.h) + (size_t)r0 * N1, n1b, rows, n1b, &bar);
-    bulk_rows(sw2, n1p, a.w2, wp, N2, n1b, &bar);
-    if (split2) bulk_rows(sw2l, n1p, a.w2lo, wp, N2, n1b, &bar);
+    bulk_rows(sh, n1p, static_cast<const T*>(a.h) + (size_t)r0 * N1, n1b, rows, n1b, &bar, 0);
+    bulk_rows(sw2, n1p, a.w2, wp, N2, n1b, &bar, 16);
+    if (split2) bulk_rows(sw2l, n1p, a.w2lo, wp, N2, n1b, &bar, 16 + N2);
   }
   for (int m = threadIdx.x; m < N2; m += blockDim.x) sb2[m] = a.b2 ? __ldg(a.b2 + m) : 0.f;
   mbar_wait(&bar, 1);
