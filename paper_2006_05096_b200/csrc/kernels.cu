@@ -1295,6 +1295,48 @@ cudaError_t flush_l2(void* buf, size_t bytes, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ im2col (fp32)
+// One thread per 4 consecutive K columns of one output pixel (a 16-byte store;
+// kpad % 32 == 0): the 3-channel fp32 stems go to the 3xTF32 tensor-core GEMM
+// over these rows instead of the FFMA conv (ResNet-50's fp32 stem was a
+// quarter of the fp32 forward).
+__global__ void im2col_f32_kernel(const float* __restrict__ x, float* __restrict__ col, long M,
+                                  int H, int W, int C, int R, int S, int stride, int pad, int OH,
+                                  int OW, int kpad) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int kq = kpad / 4;
+  if (i >= M * kq) return;
+  const long m = i / kq;
+  const int k0 = (int)(i - m * kq) * 4;
+  const int img = (int)(m / ((long)OH * OW));
+  const int rem = (int)(m - (long)img * OH * OW);
+  const int oh = rem / OW, ow = rem - oh * OW;
+  const int K = R * S * C;
+  float v[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int k = k0 + j;
+    v[j] = 0.f;
+    if (k < K) {
+      const int tap = k / C, c = k - tap * C;
+      const int r = tap / S, s2 = tap - r * S;
+      const int ih = oh * stride - pad + r, iw = ow * stride - pad + s2;
+      if ((unsigned)ih < (unsigned)H && (unsigned)iw < (unsigned)W)
+        v[j] = __ldg(x + (((size_t)img * H + ih) * W + iw) * C + c);
+    }
+  }
+  reinterpret_cast<float4*>(col)[i] = make_float4(v[0], v[1], v[2], v[3]);
+}
+
+cudaError_t im2col_f32(const float* x, float* col, int B, int H, int W, int C, int R, int S,
+                       int stride, int pad, int OH, int OW, int kpad, cudaStream_t st) {
+  const long M = (long)B * OH * OW;
+  const long n = M * (kpad / 4);
+  im2col_f32_kernel<<<nblk(n, 256), 256, 0, st>>>(x, col, M, H, W, C, R, S, stride, pad, OH, OW,
+                                                   kpad);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ fused 2-layer MLP
 // The reference's toy MLP (784 -> 256 -> act -> 10, BASELINE configs[0]) at
 // batch 1..64 is launch-bound: input pack + two GEMMs + output gather were

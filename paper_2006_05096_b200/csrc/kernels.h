@@ -157,6 +157,10 @@ struct MlpArgs {
   unsigned* counters;           // per 16-row group, zero between launches
 };
 template <typename T> cudaError_t mlp2(const MlpArgs& a, cudaStream_t st);
+// im2col rows of an NHWC fp32 conv input: col[m][k], k = (r, s, c) < R*S*C, zero
+// for k >= R*S*C up to kpad (the gathered 3xTF32 path for few-channel convs)
+cudaError_t im2col_f32(const float* x, float* col, int B, int H, int W, int C, int R, int S,
+                       int stride, int pad, int OH, int OW, int kpad, cudaStream_t st);
 template <typename T> cudaError_t gemm_simt(const GemmSimtArgs& a, cudaStream_t st);
 template <typename T>
 cudaError_t input_pack(const float* in, T* out, int B, int C, int H, int W, int Cp,

@@ -247,6 +247,8 @@ struct Layer {
   int ds_op = -1;           // 1x1 conv: index of the projection shortcut folded into its K loop
   int chain_op = -1;        // block-tail 1x1 conv: next block's 1x1 conv computed in the same kernel
   bool tf32 = false;        // fp32 plan conv/linear on the 3xTF32 tcgen05 GEMM (w = hi, w2 = lo)
+  bool tf32_gather = false; // ... with its im2col A materialised first (convs with C % 32 != 0:
+                            // the 3-channel stems), [M][kpad] fp32 in BatchState::col
   bool band8 = false;       // 3x3/s1 conv on an 8-channel padded image: conv_band CGW = 8,
                             // weights [N][r][4][8] (paired taps, 4th tap zero)
   bool fused = false;       // max-pool executed inside its producer (no launch)
@@ -267,6 +269,7 @@ struct BatchState {
   std::vector<CUtensorMap> tmR;    // per layer (tc, residual fold): residual as an A operand
   std::vector<char> fold;          // per layer: residual folded into the MMA
   unsigned* mlp_ctr = nullptr;     // fused MLP: per-16-row-group arrival counters
+  float* col = nullptr;            // gathered 3xTF32 convs: im2col A [M][kpad] fp32 (shared)
   std::vector<char> a_narrow;      // per layer: A box width for K <= 32 (0 = 64)
   std::vector<CUtensorMap> tmI;    // per layer: identity [256 x 256] (box rows = BN) for the fold
   std::vector<char> band;          // per layer: banded implicit-GEMM conv (conv_band.cu)
@@ -325,10 +328,13 @@ struct b2_plan {
   int pair_min_k = 0;        // B2_PAIR_MIN_K: shortest K sent to the CTA-pair GEMM
   bool use_pool_fusion = true;   // B2_POOL_FUSION=0 -> stem and max-pool as two kernels
   bool use_tf32 = true;          // B2_TF32=0 -> fp32 plans on the CUDA-core FFMA GEMM
+  bool tf32_gather = true;       // B2_TF32_GATHER=0 -> few-channel fp32 convs on the FFMA GEMM
   bool use_ds_fold = true;       // B2_DS_FOLD=0 -> projection shortcuts as their own kernels
   bool alt_order = true;         // B2_ALT_ORDER=0 -> every GEMM walks M tiles forward
   bool use_split = true;         // B2_SPLIT=0 -> no split-K at small batch
   bool use_chain = true;         // B2_CHAIN=0 -> block-tail and next conv1 as two GEMMs
+  bool chain_ds2 = false;        // B2_CHAIN_DS2=1 -> chain tails with a strided shortcut too
+                                 // (measured: -13 us on ResNet-50 b=256 without)
   bool use_mlp_fusion = true;    // B2_MLP_FUSE=0 -> the toy MLP as pack + 2 GEMMs + gather
   int mlp_in = -1, mlp_l1 = -1, mlp_l2 = -1, mlp_out = -1;   // fused 2-layer MLP (plan_fuse_mlp)
   int band_max_n = 128;      // B2_BAND_MAX_N: widest conv (output channels) sent to conv_band
@@ -575,6 +581,10 @@ void plan_chain(b2_plan* pl) {
       // N2 = 128: -8..-22 us) and loses once they are operand-bound (N1 = 1024:
       // +24..+89 us — every 128-column chunk re-reads its A panel)
       if (!(p[7] <= 256 || (p[7] <= 512 && q[7] <= 128))) break;
+      // a folded *strided* shortcut re-loads its im2col A panel for every
+      // 128-column O chunk (ncu, layer2 block 0: 768 KB of L2->SM operand
+      // traffic per 128-row tile, ~9 TB/s, the epilogue starved 25% of the time)
+      if (!pl->chain_ds2 && C3.ds_op >= 0 && pl->layers[C3.ds_op].p[10] != 1) break;
       C3.chain_op = (int)j;
       C1.fused = true;
       break;
@@ -685,10 +695,11 @@ int upload_weights(b2_plan* pl, const uint8_t* data, const std::vector<WeightRec
           if ((rc = upload_as<bf16>(pl, h, &L.w))) return rc;
         } else if (!bf && !pl->force_simt && pl->use_tf32 &&
                    ((plain && (conv ? L.p[6] : L.p[9]) % 4 == 0 && K % 4 == 0) ||
-                    (conv && L.p[6] % 32 == 0))) {
+                    (conv && L.p[6] % 32 == 0) || (conv && pl->tf32_gather))) {
           // 3xTF32: weights split once into hi (TF32-exact) and lo = w - hi,
           // [N][Kpad32] fp32
           L.tf32 = true;
+          L.tf32_gather = conv && !plain && L.p[6] % 32 != 0;
           L.kpad = (K + 31) / 32 * 32;
           L.ldw = L.kpad;
           std::vector<float> hi((size_t)N * L.kpad, 0.f), lo((size_t)N * L.kpad, 0.f);
@@ -906,7 +917,11 @@ int run_ops(b2_plan* pl, BatchState& S, const void* d_in, float* d_out, cudaStre
           a.act = act;
           a.tiles_m = (int)((M + 127) / 128);
           a.tiles_n = (N + 127) / 128;
-          if (!plain) {
+          if (L.tf32_gather) {   // materialise the im2col rows, then a plain GEMM over them
+            CK(im2col_f32(static_cast<const float*>(S.act[p[0]]), S.col, B, p[4], p[5], p[6], p[8],
+                          p[9], p[10], p[11], p[12], p[13], L.kpad, st));
+            ++launches;
+          } else if (!plain) {
             a.a_im2col = 1;
             a.C = p[6];
             a.R = p[8];
@@ -1357,6 +1372,7 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
   S.chain.assign(pl->layers.size(), 0);
   S.split.assign(pl->layers.size(), 1);
   size_t ws_elems = 0;
+  size_t col_elems = 0;
   S.cargs.resize(pl->layers.size());
   S.tmB2.resize(pl->layers.size());
   S.tmT.resize(pl->layers.size());
@@ -1370,6 +1386,10 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
       const long M = conv ? (long)batch * p[12] * p[13] : (long)batch * p[6];
       const bool plain = !conv || (p[8] == 1 && p[9] == 1 && p[10] == 1 && p[11] == 0);
       bool ok;
+      if (L.tf32_gather) {   // A = the materialised im2col rows
+        col_elems = std::max(col_elems, (size_t)M * L.kpad);
+        continue;            // map made once `col` exists (below)
+      }
       if (plain) {
         const long ld = conv ? p[6] : p[9];
         ok = make_tmap_f32(&S.tmA[li], S.act[p[0]], (uint64_t)M, (uint64_t)L.K,
@@ -1514,6 +1534,23 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
                                     : nar == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
                                                 : CU_TENSOR_MAP_SWIZZLE_128B))
         return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeTiled(A) failed", li);
+    }
+  }
+  if (col_elems) {
+    CK(dmalloc(pl, (void**)&S.col, col_elems * sizeof(float) + 256));
+    for (size_t li = 0; li < pl->layers.size(); ++li) {
+      const Layer& L = pl->layers[li];
+      if (!L.tf32_gather) continue;
+      const int* p = L.p;
+      const int N = p[7];
+      const long M = (long)batch * p[12] * p[13];
+      if (!make_tmap_f32(&S.tmA[li], S.col, (uint64_t)M, (uint64_t)L.kpad, (uint64_t)L.kpad * 4,
+                         128) ||
+          !make_tmap_f32(&S.tmB[li], L.w, (uint64_t)N, (uint64_t)L.kpad, (uint64_t)L.kpad * 4,
+                         128) ||
+          !make_tmap_f32(&S.tmI[li], L.w2, (uint64_t)N, (uint64_t)L.kpad, (uint64_t)L.kpad * 4,
+                         128))
+        return fail(B2_ERR_CUDA, "layer %zu: gathered 3xTF32 tensor maps rejected", li);
     }
   }
   if (ws_elems) {
@@ -1666,10 +1703,12 @@ int b2_plan_create(const void* blob, size_t len, int dtype, b2_plan** out) {
   if (const char* pk = knob("B2_PAIR_MIN_K")) pl->pair_min_k = atoi(pk);
   if (const char* pf = knob("B2_POOL_FUSION")) pl->use_pool_fusion = pf[0] != '0';
   if (const char* tf = knob("B2_TF32")) pl->use_tf32 = tf[0] != '0';
+  if (const char* tg = knob("B2_TF32_GATHER")) pl->tf32_gather = tg[0] != '0';
   if (const char* df = knob("B2_DS_FOLD")) pl->use_ds_fold = df[0] != '0';
   if (const char* ao = knob("B2_ALT_ORDER")) pl->alt_order = ao[0] != '0';
   if (const char* sk = knob("B2_SPLIT")) pl->use_split = sk[0] != '0';
   if (const char* cz = knob("B2_CHAIN")) pl->use_chain = cz[0] != '0';
+  if (const char* cd = knob("B2_CHAIN_DS2")) pl->chain_ds2 = cd[0] != '0';
   if (const char* mf = knob("B2_MLP_FUSE")) pl->use_mlp_fusion = mf[0] != '0';
   if (const char* bm = knob("B2_BAND_MAX_N")) pl->band_max_n = atoi(bm);
   const auto tv0 = std::chrono::steady_clock::now();
@@ -2028,6 +2067,7 @@ void b2_plan_destroy(b2_plan* pl) {
     if (S.graph2) cudaGraphExecDestroy(S.graph2);
     if (S.ws) cudaFree(S.ws);
     if (S.mlp_ctr) cudaFree(S.mlp_ctr);
+    if (S.col) cudaFree(S.col);
     if (S.d_in2) cudaFree(S.d_in2);
     if (S.d_out2) cudaFree(S.d_out2);
     if (S.h_out2) cudaFreeHost(S.h_out2);
