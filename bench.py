@@ -173,7 +173,8 @@ def roofline(plan, model: str, batch: int, ms_per_step: float, pk: dict) -> dict
     true channel counts: 8.178 GFLOP/sample for ResNet-50) x
     batch, divided by the time those kernels take per step = the CUDA-graph
     step time measured in this run x their share of the forward in the
-    committed ncu launch list (profiles/ncu_traffic.json, same model/batch).
+    committed ncu launch list (profiles/ncu_traffic.json from
+    tools/ncu_traffic_json.py, same model/batch).
     ``frac_whole_step`` charges the whole step (every kernel) instead.  Peak =
     the measured BURST bf16 figure (a ~3 ms forward replayed for < 1 s runs
     at boost clocks, not under the sustained power cap)."""

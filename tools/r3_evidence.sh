@@ -2,13 +2,12 @@
 # (ResNet-50 b=256, BERT b=128), per-model op profiles, the full GPU suite, bench line, C4 sweep.
 cd $GRAFT_REPO_ROOT
 E=gpurun_out/ev; mkdir -p $E
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $E/launches.csv python bench.py --steps 2 --warmup 3 --no-sweep --no-cpu > /dev/null 2>&1
-python tools/ncu_launches.py $E/launches.csv $E/launch_summary.txt $E/ncu_traffic.json > /dev/null 2>&1
-cp $E/ncu_traffic.json profiles/ncu_traffic.json 2>/dev/null
 M=gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,dram__bytes_read.sum,dram__bytes_write.sum,l1tex__m_xbar2l1tex_read_bytes.sum
 timeout 600 ncu --metrics $M --clock-control none --csv --log-file $E/lm_r50.csv python tools/ncu_target.py resnet50 256 > /dev/null 2>&1
 timeout 600 ncu --metrics $M --clock-control none --csv --log-file $E/lm_bert.csv python tools/ncu_target.py bert 128 > /dev/null 2>&1
 python tools/ncu_launch_table.py $E/lm_r50.csv $E/launch_table_resnet50.txt > /dev/null 2>&1
+python tools/ncu_traffic_json.py $E/lm_r50.csv $E/ncu_traffic.json > /dev/null 2>&1
+cp $E/ncu_traffic.json profiles/ncu_traffic.json   # bench.py below reads it
 python tools/ncu_launch_table.py $E/lm_bert.csv $E/launch_table_bert.txt embed_ln > /dev/null 2>&1
 for m in "resnet50 256" "bert 128" "vgg16 256" "mobilenet_v2 256"; do
   set -- $m; timeout 300 python tools/profile_ops.py $1 $2 1 > $E/ops_$1.txt 2>&1
