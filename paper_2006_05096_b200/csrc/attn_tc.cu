@@ -98,6 +98,14 @@ __global__ void __launch_bounds__(AT_WARPS * 32, AT_CTAS_PER_SM)
   const uint32_t trow = tbase + (uint32_t(q * 32) << 16) + hh * 64;   // this thread's 64 scores
   int it = 0;
   for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+    // key-validity bits (attention mask) fetched before the waits: on the
+    // critical path (after S) the L2 round trip was ~5% of the kernel's stalls
+    uint32_t w0 = 0xffffffffu, w1 = 0xffffffffu;
+    if (keymask) {
+      const int bq = u / H;
+      w0 = __ldg(keymask + bq * 4 + hh * 2);
+      w1 = __ldg(keymask + bq * 4 + hh * 2 + 1);
+    }
     mbar_wait(&bars[0], it & 1);
     __syncwarp();
     tc_fence_after();
@@ -115,12 +123,6 @@ __global__ void __launch_bounds__(AT_WARPS * 32, AT_CTAS_PER_SM)
     tc_fence_after();
 
     // ---- softmax over this thread's row, key half hh (64 scores, two 32-column passes)
-    uint32_t w0 = 0xffffffffu, w1 = 0xffffffffu;   // key-validity bits (attention mask)
-    if (keymask) {
-      const int bq = u / H;
-      w0 = __ldg(keymask + bq * 4 + hh * 2);
-      w1 = __ldg(keymask + bq * 4 + hh * 2 + 1);
-    }
     float sv[32];
     auto load_half = [&](int half) {   // 32 scores; padded keys -> float32 min (exp2 underflows)
       uint32_t r[32];
