@@ -56,7 +56,11 @@ __global__ void __launch_bounds__(CH_THREADS, 1)
   uint8_t* sRing = smem;                                   // ST x (A 16 KB | B1 16 KB)
   uint8_t* sA2 = sRing + ST * CH_STAGE;                    // 2 x O chunk (32 KB each)
   uint8_t* sB2 = sA2 + 2 * CH_A2_BYTES;                    // S2 x (N2 x 64) weights
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB2 + S2 * B2_BYTES);
+  // T1 staging of its own (N2 / 64 blocks of 16 KB): the T1 epilogue no longer
+  // drains every outstanding O store before reusing the O buffers, and no
+  // longer waits for its own store before the next tile's first O chunk
+  uint8_t* sT = sB2 + S2 * B2_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sT + (a.N2 / 64) * CH_A_BYTES);
   uint64_t* empty = full + ST;
   uint64_t* b2full = empty + ST;
   uint64_t* b2empty = b2full + S2;
@@ -324,13 +328,18 @@ __global__ void __launch_bounds__(CH_THREADS, 1)
           bulk_commit();
         }
       }
-      // ---- T1 = relu(acc2 + b1): staged through buffer g & 1 (the next chunk's)
+      // ---- T1 = relu(acc2 + b1), staged in sT.  Bulk groups retire in order:
+      // with this tile's C O-chunk stores still allowed in flight, the previous
+      // tile's T1 store has been read out of sT.
       mbar_wait(t2full, tt & 1);
       tc_fence_after();
-      const int buf = g & 1;
-      if (issuer) bulk_wait_read<0>();
+      if (issuer) {
+        if (C >= 4) bulk_wait_read<4>();
+        else if (C == 3) bulk_wait_read<3>();
+        else if (C == 2) bulk_wait_read<2>();
+        else bulk_wait_read<1>();
+      }
       chain_bar();
-      uint8_t* dst = sA2 + buf * CH_A2_BYTES;
       for (int kb = 0; kb < a.N2 / 64; ++kb) {
         const int col = kb * 64 + eh * 32;
         uint32_t r[32];
@@ -346,8 +355,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1)
           bv[4 * j + 3] = b4.w;
         }
         tmem_wait_ld();
-        // K block kb of T1 goes to 16 KB slot kb (N2 <= 256: up to 4 slots = 2 chunk buffers)
-        uint8_t* rowp = sA2 + ((buf * 2 + kb) % 4) * CH_A_BYTES + row * 128;
+        uint8_t* rowp = sT + kb * CH_A_BYTES + row * 128;   // K block kb of T1
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           uint4 w;
@@ -370,11 +378,9 @@ __global__ void __launch_bounds__(CH_THREADS, 1)
       chain_bar();
       if (issuer) {
         for (int kb = 0; kb < a.N2 / 64; ++kb)
-          tma_store_2d(&tmT, sA2 + ((buf * 2 + kb) % 4) * CH_A_BYTES, kb * CH_BK, m0);
+          tma_store_2d(&tmT, sT + kb * CH_A_BYTES, kb * CH_BK, m0);
         bulk_commit();
-        bulk_wait_read<0>();   // staging reused by the next tile's chunks
       }
-      chain_bar();
     }
     if (issuer) bulk_wait<0>();
   }
@@ -389,6 +395,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1)
 
 static int chain_smem(const ChainArgs& a) {
   return 1024 + a.stages * CH_STAGE + 2 * CH_A2_BYTES + a.b2_stages * a.N2 * CH_BK * 2 +
+         (a.N2 / 64) * CH_A_BYTES +
          8 * (2 * a.stages + 2 * a.b2_stages + 10) + 16;
 }
 

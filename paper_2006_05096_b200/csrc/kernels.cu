@@ -766,8 +766,44 @@ __global__ void avgpool_kernel(const T* __restrict__ x, T* __restrict__ y, int B
   for (int q = 0; q < HW; ++q) s += to_f(p[(long)q * C]);
   y[i] = from_f<T>(s / HW);
 }
+// bf16, C % 8 == 0: a thread sums 8 channels with 16-byte loads (same per-channel
+// order as the scalar kernel: bit-identical); the scalar version's 2-byte loads
+// ran ResNet-50's 51 MB average pool at 2.9 TB/s
+__global__ void avgpool8_kernel(const bf16* __restrict__ x, bf16* __restrict__ y, int B, int HW,
+                                int C) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;   // over B * C / 8
+  const int c8 = C / 8;
+  if (i >= (long)B * c8) return;
+  const long b = i / c8;
+  const int c = (int)(i - b * c8) * 8;
+  const bf16* p = x + b * HW * (long)C + c;
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 7
+  for (int q = 0; q < HW; ++q) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(p + (long)q * C));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const float2 f = unpack_bf16x2(w[h]);
+      s[2 * h] += f.x;
+      s[2 * h + 1] += f.y;
+    }
+  }
+  uint32_t o[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) o[h] = pack_bf16x2(s[2 * h] / HW, s[2 * h + 1] / HW);
+  reinterpret_cast<uint4*>(y + b * C + c)[0] = make_uint4(o[0], o[1], o[2], o[3]);
+}
+
 template <typename T>
 cudaError_t avgpool(const T* x, T* y, int B, int HW, int C, cudaStream_t st) {
+  if constexpr (sizeof(T) == 2) {
+    if (C % 8 == 0) {
+      avgpool8_kernel<<<nblk((long)B * C / 8, 128), 128, 0, st>>>(
+          reinterpret_cast<const bf16*>(x), reinterpret_cast<bf16*>(y), B, HW, C);
+      return cudaGetLastError();
+    }
+  }
   avgpool_kernel<T><<<nblk((long)B * C, 256), 256, 0, st>>>(x, y, B, HW, C);
   return cudaGetLastError();
 }
