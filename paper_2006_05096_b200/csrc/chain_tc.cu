@@ -34,7 +34,6 @@ constexpr int CH_A_BYTES = CH_BM * CH_BK * 2;        // 16 KB
 constexpr int CH_B1_BYTES = CH_BN * CH_BK * 2;       // 16 KB
 constexpr int CH_STAGE = CH_A_BYTES + CH_B1_BYTES;
 constexpr int CH_A2_BYTES = CH_BM * CH_BN * 2;       // one O chunk: 2 K blocks of 16 KB
-constexpr int CH_ID_BYTES = 64 * CH_BK * 2;          // residual fold: 64 x 64 identity (8 KB)
 
 B2_DEV void chain_bar() { asm volatile("bar.sync 1, %0;" ::"n"(CH_EPI_WARPS * 32) : "memory"); }
 
@@ -138,16 +137,15 @@ __global__ void __launch_bounds__(CH_THREADS, 1)
           const uint32_t dB = dA + CH_A_BYTES;
           const uint32_t fb = full_lo + st * 8;
           if (elect_one()) {
-            mbar_arrive_expect_tx_u32(fb, kb >= kblocks && fold == 0 ? CH_A_BYTES + CH_ID_BYTES
-                                                                     : CH_STAGE);
+            mbar_arrive_expect_tx_u32(fb, CH_STAGE);
             if (kb < kblocks) {
               tma_load_2d_u32(dA, &tmA, fb, kb * CH_BK, m0);
               tma_load_2d_u32(dB, &tmB1, fb, kb * CH_BK, n0);
             } else {
               const int j = kb - kblocks;
-              if (fold == 0) {                  // residual block j x a 64 x 64 identity
+              if (fold == 0) {                  // residual x identity
                 tma_load_2d_u32(dA, &tmR, fb, n0 + j * CH_BK, m0);
-                tma_load_2d_u32(dB, &tmI, fb, 0, 0);
+                tma_load_2d_u32(dB, &tmI, fb, j * CH_BK, 0);
               } else {                          // projection shortcut x Wd
                 if (fold == 1)
                   tma_load_2d_u32(dA, &tmR, fb, j * CH_BK, m0);
@@ -200,8 +198,6 @@ __global__ void __launch_bounds__(CH_THREADS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc1 = make_idesc(CH_BM, CH_BN, 1u);
-    constexpr uint32_t idesc_id = make_idesc(CH_BM, 64, 1u);   // residual-fold blocks
-    const int kmain = a.fold_kind == 0 ? a.kblocks : KT1;
     const uint32_t idesc2 = make_idesc(CH_BM, a.N2, 1u);
     int st = 0, s2 = 0;
     uint32_t ph = 0, ph2 = 0;
@@ -217,16 +213,9 @@ __global__ void __launch_bounds__(CH_THREADS, 1)
         tc_fence_after();
         const uint64_t ad = smem_desc_sw128(smem_u32(sRing + st * CH_STAGE));
         const uint64_t bd = smem_desc_sw128(smem_u32(sRing + st * CH_STAGE + CH_A_BYTES));
-        if (kb < kmain) {
 #pragma unroll
-          for (int k = 0; k < CH_BK / 16; ++k)
-            if (elect_one()) umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc1, (kb | k) != 0 ? 1u : 0u);
-        } else {   // residual block j: accumulator columns [64 j, 64 j + 64) only
-          const uint32_t dj = d + (uint32_t)(kb - kmain) * 64;
-#pragma unroll
-          for (int k = 0; k < CH_BK / 16; ++k)
-            if (elect_one()) umma_bf16(dj, ad + 2 * k, bd + 2 * k, idesc_id, 1u);
-        }
+        for (int k = 0; k < CH_BK / 16; ++k)
+          if (elect_one()) umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc1, (kb | k) != 0 ? 1u : 0u);
         if (elect_one()) umma_commit(&empty[st]);
         if (++st == ST) {
           st = 0;

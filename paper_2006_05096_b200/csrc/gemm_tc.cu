@@ -727,8 +727,6 @@ __global__ void __launch_bounds__(TcCfg<BN, GATHER>::THREADS, 1)
 // it, the leader alone expects 2 x stage bytes); empty[s] and tfull[] exist in
 // both CTAs and receive the leader's multicast commits; the leader's
 // tempty[] collects the epilogue warps of both CTAs (16 arrivals).
-constexpr int TC2_ID_BYTES = 32 * TC_BK * 2;   // pair residual fold: 32 identity rows per CTA
-
 template <int BN>
 struct Tc2Cfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
@@ -840,15 +838,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<BN>::THREADS,
         const uint32_t dA = sA_lo + stage * Cfg::A_BYTES;
         const uint32_t dB = sB_lo + stage * Cfg::B_BYTES;
         if (elect_one()) {
-          const bool rfold = kb >= kblocks && fold == 0;
-          if (urank == 0)
-            mbar_arrive_expect_tx_u32(full_lo + stage * 8,
-                                      rfold ? 2 * (Cfg::A_BYTES + TC2_ID_BYTES) : 2 * Cfg::STAGE_BYTES);
+          if (urank == 0) mbar_arrive_expect_tx_u32(full_lo + stage * 8, 2 * Cfg::STAGE_BYTES);
           if (kb >= kblocks) {
             const int j = kb - kblocks;
-            if (fold == 0) {   // residual block j x a 64 x 64 identity (this CTA's 32 rows of it)
+            if (fold == 0) {   // residual x identity (this CTA's half of the rows)
               tma_load_2d_pair_u32(dA, &tmR, fl, n0 + j * TC_BK, m0);
-              tma_load_2d_pair_u32(dB, &tmI, fl, 0, urank * 32);
+              tma_load_2d_pair_u32(dB, &tmI, fl, j * TC_BK, urank * (BN / 2));
             } else {           // folded projection shortcut: x (or strided x) x Wd
               if (fold == 1)
                 tma_load_2d_pair_u32(dA, &tmR, fl, j * TC_BK, m0);
@@ -883,8 +878,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<BN>::THREADS,
     // ------------------------------------------------------------ MMA issuer (leader, whole warp)
     if (rank == 0) {
       constexpr uint32_t idesc = make_idesc(2 * TC_BM, BN, 1u);
-      constexpr uint32_t idesc_id = make_idesc(2 * TC_BM, 64, 1u);   // residual-fold blocks
-      const int kmain = a.fold_kind == 0 ? a.kblocks : KT;
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -898,20 +891,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<BN>::THREADS,
           tc_fence_after();
           const uint64_t ad = smem_desc_sw128(smem_u32(sA + stage * Cfg::A_BYTES));
           const uint64_t bd = smem_desc_sw128(smem_u32(sB + stage * Cfg::B_BYTES));
-          if (kb < kmain) {
 #pragma unroll
-            for (int k = 0; k < TC_BK / 16; ++k)
-              if (elect_one())
-                umma_bf16_pair(dt, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
-          } else {
-            // residual fold: block j lands on accumulator columns [64 j, 64 j + 64) only
-            // (N = 64 MMA against a 64 x 64 identity, not an N = BN one against
-            // BN identity rows that are zero outside that window)
-            const uint32_t dj = dt + (uint32_t)(kb - kmain) * 64;
-#pragma unroll
-            for (int k = 0; k < TC_BK / 16; ++k)
-              if (elect_one()) umma_bf16_pair(dj, ad + 2 * k, bd + 2 * k, idesc_id, 1u);
-          }
+          for (int k = 0; k < TC_BK / 16; ++k)
+            if (elect_one()) umma_bf16_pair(dt, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
           if (elect_one()) umma_commit_pair(&empty[stage]);
           if (++stage == ST) {
             stage = 0;

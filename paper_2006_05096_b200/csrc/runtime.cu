@@ -1167,7 +1167,7 @@ int plan_chain_state(b2_plan* pl, BatchState& S, size_t li, int batch) {
   } else {
     ok = ok && make_tmap_bf16(&S.tmR[li], S.act[p[15]], (uint64_t)M, (uint64_t)N1,
                               (uint64_t)N1 * 2, 128) &&
-         make_tmap_bf16(&S.tmI[li], pl->identity, 256, 256, 512, 64);   // 64 x 64 window
+         make_tmap_bf16(&S.tmI[li], pl->identity, 256, 256, 512, 128);
     a.res_kblocks = 2;             // 128 residual columns per O chunk
     a.fold_kind = 0;
   }
@@ -1510,7 +1510,7 @@ int get_state(b2_plan* pl, int batch, BatchState** out) {
                S.split[li] == 1) {   // split-K adds the residual in its finalize pass
       if (!make_tmap_bf16(&S.tmR[li], S.act[res_t], (uint64_t)M, (uint64_t)N, (uint64_t)N * 2,
                           128) ||
-          !make_tmap_bf16(&S.tmI[li], pl->identity, 256, 256, 512, pair_ok ? 32 : bbox))
+          !make_tmap_bf16(&S.tmI[li], pl->identity, 256, 256, 512, bbox))
         return fail(B2_ERR_CUDA, "layer %zu: cuTensorMapEncodeTiled(res/identity) failed", li);
       S.fold[li] = 1;
     }
