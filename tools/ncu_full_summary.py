@@ -1,0 +1,37 @@
+"""Key counters of `ncu --set full` captures (one kernel each), for profiles/.
+usage: ncu_full_summary.py <rep.ncu-rep> [...]"""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe active (% of active)"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe active (% of elapsed)"),
+    ("sm__cycles_active.avg", "SM active cycles (avg)"),
+    ("sm__cycles_elapsed.avg", "SM elapsed cycles (avg)"),
+    ("l1tex__m_xbar2l1tex_read_bytes.sum", "L2 -> SM bytes"),
+    ("l1tex__m_xbar2l1tex_read_bytes.sum.pct_of_peak_sustained_elapsed", "L2 -> SM (% of peak)"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput (% of peak)"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput (% of peak)"),
+    ("launch__grid_size", "grid"),
+    ("launch__registers_per_thread", "registers / thread"),
+]
+
+for rep in sys.argv[1:]:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    if len(rows) < 3:
+        print(f"{rep}: no data")
+        continue
+    h, u, v = rows[0], rows[1], rows[2]
+    name = v[h.index("Kernel Name")] if "Kernel Name" in h else "?"
+    print(f"## {rep.split('/')[-1]}: {name[:110]}")
+    for k, label in KEYS:
+        if k in h:
+            i = h.index(k)
+            print(f"  {label:40s} {v[i]:>14s} {u[i]}")
+    print()

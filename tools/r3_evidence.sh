@@ -17,3 +17,7 @@ tail -3 $E/gputests.log
 timeout 900 python bench.py > $E/bench.json 2> $E/bench.err
 python -c "import json;d=json.loads(open('$E/bench.json').read());print(d['value'],d['ms_per_step'],d['e2e']['value'],d['roofline']['frac'],d.get('sweep_c4',{}).get('wall_s'))"
 timeout 900 python tools/sweep_bench.py $E/sweep_c4 > $E/sweep.log 2>&1; tail -2 $E/sweep.log
+# one --set full capture each of the dominant kernels (CTA-pair GEMM, chain) at the bench config
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:tc_gemm2 -s 12 -c 1 -o $E/gemm2_full python tools/ncu_target.py resnet50 256 > /dev/null 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:chain_gemm -s 1 -c 1 -o $E/chain_full python tools/ncu_target.py resnet50 256 > /dev/null 2>&1
+ls -la $E/*.ncu-rep
