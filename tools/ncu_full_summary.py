@@ -17,6 +17,8 @@ KEYS = [
     ("dram__bytes_write.sum", "DRAM write"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput (% of peak)"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput (% of peak)"),
+    ("sm__inst_executed.avg.per_cycle_active", "IPC (per SM, active)"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy (%)"),
     ("launch__grid_size", "grid"),
     ("launch__registers_per_thread", "registers / thread"),
 ]
