@@ -57,26 +57,70 @@ def peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock / clock-event (throttle) reasons sampled DURING a timed region:
+    NVML polled every 2 ms in a thread (a 20-step ResNet-50 region lasts
+    ~60 ms, one nvidia-smi call ~50-100 ms), nvidia-smi as the fallback."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap,utilization.gpu")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
-        self.rows: list[list[str]] = []
+        self.rows: list[tuple] = []     # (sm_mhz, max_mhz, [4 reason flags], util %)
+        self.source = "nvml"
         self._halt = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
+    def _run_nvml(self) -> bool:
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = None
+            try:   # the CUDA device this process runs on (NVML ignores CUDA_VISIBLE_DEVICES)
+                import torch
+                pr = torch.cuda.get_device_properties(self.index)
+                bus = "%08X:%02X:%02X.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+                h = N.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = None
+            if h is None:
+                h = N.nvmlDeviceGetHandleByIndex(self.index)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                    N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+        except Exception:
+            return False
+        try:
+            while not self._halt.is_set():
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                u = N.nvmlDeviceGetUtilizationRates(h).gpu
+                self.rows.append((float(sm), float(mx), [bool(r & b) for b in bits], int(u)))
+                self._halt.wait(0.002)
+        finally:
+            try:
+                N.nvmlShutdown()
+            except Exception:
+                pass
+        return True
+
     def _run(self):
+        if self._run_nvml():
+            return
+        self.source = "nvidia-smi"
         while not self._halt.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index),
                                       f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
                                      capture_output=True, text=True, timeout=5).stdout
                 for line in out.strip().splitlines():
-                    self.rows.append([c.strip() for c in line.split(",")])
+                    c = [x.strip() for x in line.split(",")]
+                    self.rows.append((float(c[0]) if c[0].replace(".", "").isdigit() else None,
+                                      float(c[1]) if c[1].replace(".", "").isdigit() else None,
+                                      [c[2 + i] == "Active" for i in range(4)],
+                                      int(c[6]) if c[6].isdigit() else 0))
             except Exception:
                 return
             self._halt.wait(0.2)
@@ -89,16 +133,22 @@ class ClockSampler:
         self._halt.set()
         self._t.join(timeout=6)
 
-    def summary(self) -> dict:
-        if not self.rows:
+    @staticmethod
+    def summary_of(samplers) -> dict:
+        rows = [r for s in samplers for r in s.rows]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        busy = [r for r in self.rows if r[6].isdigit() and int(r[6]) > 0] or self.rows
-        sm = [float(r[0]) for r in busy if r[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in busy for i in range(4) if r[2 + i] == "Active"})
+        busy = [r for r in rows if r[3] > 0] or rows
+        sm = [r[0] for r in busy if r[0] is not None]
+        reasons = sorted({ClockSampler.NAMES[i] for r in busy for i in range(4) if r[2][i]})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].isdigit() else None,
-                "reasons": reasons, "samples": len(busy)}
+                "sm_min_mhz": min(sm) if sm else None,
+                "sm_max_mhz": rows[0][1], "reasons": reasons, "samples": len(busy),
+                "source": samplers[0].source,
+                "regions": "device-timed and e2e-timed regions"}
+
+    def summary(self) -> dict:
+        return self.summary_of([self])
 
 
 def build_plan(model: str, dtype: int) -> bytes:
@@ -345,7 +395,8 @@ def run_ours(args) -> dict | None:
     # end-to-end through the C ABI with host buffers (pinned H2D + D2H per step)
     plan.bench(B, 1, 1, seed=2, e2e=True)
     barrier()
-    elat, ecomp = plan.bench(B, K, W, seed=0, e2e=True)
+    with ClockSampler(0 if world > 1 else int(os.environ.get("B2_GPU_INDEX", "0"))) as clk_e2e:
+        elat, ecomp = plan.bench(B, K, W, seed=0, e2e=True)
     barrier()
     e2e_ms = max_over_ranks(float(ecomp[-1]))
     e2e_value = world * K * B / (e2e_ms / 1e3)
@@ -379,7 +430,7 @@ def run_ours(args) -> dict | None:
                 "mode": "b2_bench_e2e: pinned fp32 inputs H2D + forward + logits D2H every step, "
                         "software-pipelined over 3 streams (H2D i+1 and D2H i-1 overlap forward i)"},
         "gpu_launches": int(K * plan.launches_per_forward),
-        "clocks": clk.summary(),
+        "clocks": ClockSampler.summary_of([clk, clk_e2e]),
     }
     if sweep is not None:
         line["sweep_c4"] = sweep
