@@ -69,6 +69,11 @@ B2_DEV uint64_t f2mul(uint64_t a, uint64_t b) {
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+B2_DEV uint64_t f2add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 B2_DEV void gelu_erf2(float& va, float& vb) {
   const float c = 0.70710678118654752f;
   const uint64_t z = f2pack(fabsf(va) * c, fabsf(vb) * c);
@@ -85,9 +90,9 @@ B2_DEV void gelu_erf2(float& va, float& vb) {
   r = f2mul(r, r);
   r = f2mul(r, r);
   r = f2mul(r, r);
-  float ra, rb;
-  f2unpack(r, ra, rb);
-  const float ea = copysignf(1.f - ra, va), eb = copysignf(1.f - rb, vb);
+  float ra, rb;   // 1 - r as one packed fma (single rounding, same as the scalar subtract)
+  f2unpack(f2fma(r, f2pack(-1.f, -1.f), f2pack(1.f, 1.f)), ra, rb);
+  const float ea = copysignf(ra, va), eb = copysignf(rb, vb);
   const uint64_t h = f2mul(f2pack(va, vb), f2pack(0.5f, 0.5f));
   float oa, ob;
   f2unpack(f2fma(h, f2pack(ea, eb), h), oa, ob);

@@ -183,7 +183,10 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint
       tmem_wait_ld();
       float v[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + bv[j];
+      for (int j = 0; j < 16; ++j)   // + bias on packed pairs (add.rn.f32x2: per-lane identical)
+        f2unpack(f2add(f2pack(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])),
+                       f2pack(bv[2 * j], bv[2 * j + 1])),
+                 v[2 * j], v[2 * j + 1]);
       if (has_res) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) add_bf16x8(v + 8 * q, rcur[q]);

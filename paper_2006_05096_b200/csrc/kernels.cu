@@ -937,11 +937,6 @@ __global__ void __launch_bounds__(256) layernorm_vec_kernel(const bf16* __restri
 // f32x2 pairs in registers and walks rows r, r + nwarps, ... with the next
 // row's 48 bytes per lane prefetched; sums, centring, scaling and the affine
 // run on packed fma/mul/add.rn.f32x2 (FFMA2 ...): ~5 instructions per element.
-B2_DEV uint64_t f2add(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
 B2_DEV uint64_t bf16x2_to_f2(uint32_t w) {   // (lo, hi) bf16 pair -> (f32, f32)
   return f2pack(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
 }
