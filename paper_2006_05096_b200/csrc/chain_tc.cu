@@ -37,6 +37,8 @@ constexpr int CH_A2_BYTES = CH_BM * CH_BN * 2;       // one O chunk: 2 K blocks 
 
 B2_DEV void chain_bar() { asm volatile("bar.sync 1, %0;" ::"n"(CH_EPI_WARPS * 32) : "memory"); }
 
+B2_DEV uint32_t relu_pack2(float2 s) { return pack_bf16x2(fmaxf(s.x, 0.f), fmaxf(s.y, 0.f)); }
+
 B2_DEV int chain_mtile(const ChainArgs& a, int t) { return a.reverse ? a.tiles_m - 1 - t : t; }
 
 __global__ void __launch_bounds__(CH_THREADS, 1)
@@ -302,14 +304,10 @@ __global__ void __launch_bounds__(CH_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             uint4 w;
-            w.x = pack_bf16x2(fmaxf(__uint_as_float(r[8 * j + 0]) + bv[8 * j + 0], 0.f),
-                              fmaxf(__uint_as_float(r[8 * j + 1]) + bv[8 * j + 1], 0.f));
-            w.y = pack_bf16x2(fmaxf(__uint_as_float(r[8 * j + 2]) + bv[8 * j + 2], 0.f),
-                              fmaxf(__uint_as_float(r[8 * j + 3]) + bv[8 * j + 3], 0.f));
-            w.z = pack_bf16x2(fmaxf(__uint_as_float(r[8 * j + 4]) + bv[8 * j + 4], 0.f),
-                              fmaxf(__uint_as_float(r[8 * j + 5]) + bv[8 * j + 5], 0.f));
-            w.w = pack_bf16x2(fmaxf(__uint_as_float(r[8 * j + 6]) + bv[8 * j + 6], 0.f),
-                              fmaxf(__uint_as_float(r[8 * j + 7]) + bv[8 * j + 7], 0.f));
+            w.x = relu_pack2(acc_add2(r[8 * j + 0], r[8 * j + 1], bv[8 * j + 0], bv[8 * j + 1]));
+            w.y = relu_pack2(acc_add2(r[8 * j + 2], r[8 * j + 3], bv[8 * j + 2], bv[8 * j + 3]));
+            w.z = relu_pack2(acc_add2(r[8 * j + 4], r[8 * j + 5], bv[8 * j + 4], bv[8 * j + 5]));
+            w.w = relu_pack2(acc_add2(r[8 * j + 6], r[8 * j + 7], bv[8 * j + 6], bv[8 * j + 7]));
             const uint32_t chunk16 = (uint32_t)(eh * 4 + j);   // 16-byte chunk in the 128-byte row
             *reinterpret_cast<uint4*>(rowp + ((chunk16 ^ sw) << 4)) = w;
           }
@@ -359,14 +357,10 @@ __global__ void __launch_bounds__(CH_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           uint4 w;
-          w.x = pack_bf16x2(fmaxf(__uint_as_float(r[8 * j + 0]) + bv[8 * j + 0], 0.f),
-                            fmaxf(__uint_as_float(r[8 * j + 1]) + bv[8 * j + 1], 0.f));
-          w.y = pack_bf16x2(fmaxf(__uint_as_float(r[8 * j + 2]) + bv[8 * j + 2], 0.f),
-                            fmaxf(__uint_as_float(r[8 * j + 3]) + bv[8 * j + 3], 0.f));
-          w.z = pack_bf16x2(fmaxf(__uint_as_float(r[8 * j + 4]) + bv[8 * j + 4], 0.f),
-                            fmaxf(__uint_as_float(r[8 * j + 5]) + bv[8 * j + 5], 0.f));
-          w.w = pack_bf16x2(fmaxf(__uint_as_float(r[8 * j + 6]) + bv[8 * j + 6], 0.f),
-                            fmaxf(__uint_as_float(r[8 * j + 7]) + bv[8 * j + 7], 0.f));
+          w.x = relu_pack2(acc_add2(r[8 * j + 0], r[8 * j + 1], bv[8 * j + 0], bv[8 * j + 1]));
+          w.y = relu_pack2(acc_add2(r[8 * j + 2], r[8 * j + 3], bv[8 * j + 2], bv[8 * j + 3]));
+          w.z = relu_pack2(acc_add2(r[8 * j + 4], r[8 * j + 5], bv[8 * j + 4], bv[8 * j + 5]));
+          w.w = relu_pack2(acc_add2(r[8 * j + 6], r[8 * j + 7], bv[8 * j + 6], bv[8 * j + 7]));
           const uint32_t chunk16 = (uint32_t)(eh * 4 + j);
           *reinterpret_cast<uint4*>(rowp + ((chunk16 ^ sw) << 4)) = w;
         }

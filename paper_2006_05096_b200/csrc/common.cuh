@@ -74,6 +74,13 @@ B2_DEV uint64_t f2add(uint64_t a, uint64_t b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+// accumulator pair (raw tcgen05.ld words) + bias pair on one add.rn.f32x2
+// (per-lane identical to the two scalar adds; half the issue slots)
+B2_DEV float2 acc_add2(uint32_t a0, uint32_t a1, float b0, float b1) {
+  float x, y;
+  f2unpack(f2add(f2pack(__uint_as_float(a0), __uint_as_float(a1)), f2pack(b0, b1)), x, y);
+  return make_float2(x, y);
+}
 B2_DEV void gelu_erf2(float& va, float& vb) {
   const float c = 0.70710678118654752f;
   const uint64_t z = f2pack(fabsf(va) * c, fabsf(vb) * c);

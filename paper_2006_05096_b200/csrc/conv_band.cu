@@ -502,8 +502,11 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
           for (int j = 0; j < 4; ++j) {
             float v[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              v[e] = act_t<ACT>(__uint_as_float(rr[8 * j + e]) + bv[8 * j + e]);
+            for (int e = 0; e < 8; e += 2) {
+              const float2 a2 = acc_add2(rr[8 * j + e], rr[8 * j + e + 1], bv[8 * j + e], bv[8 * j + e + 1]);
+              v[e] = act_t<ACT>(a2.x);
+              v[e + 1] = act_t<ACT>(a2.y);
+            }
             uint4 w;
             w.x = pack_bf16x2(v[0], v[1]);
             w.y = pack_bf16x2(v[2], v[3]);
@@ -742,8 +745,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CB_THREADS, 1)
           for (int j = 0; j < 4; ++j) {
             float v[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              v[e] = act_t<ACT>(__uint_as_float(rr[8 * j + e]) + bpre[8 * j + e]);
+            for (int e = 0; e < 8; e += 2) {
+              const float2 a2 =
+                  acc_add2(rr[8 * j + e], rr[8 * j + e + 1], bpre[8 * j + e], bpre[8 * j + e + 1]);
+              v[e] = act_t<ACT>(a2.x);
+              v[e + 1] = act_t<ACT>(a2.y);
+            }
             uint4 w;
             w.x = pack_bf16x2(v[0], v[1]);
             w.y = pack_bf16x2(v[2], v[3]);
@@ -1142,7 +1149,11 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
             uint4 w;
             float v[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) v[e] = fmaxf(__uint_as_float(rr[8 * j + e]) + bv[8 * j + e], 0.f);
+            for (int e = 0; e < 8; e += 2) {
+              const float2 a2 = acc_add2(rr[8 * j + e], rr[8 * j + e + 1], bv[8 * j + e], bv[8 * j + e + 1]);
+              v[e] = fmaxf(a2.x, 0.f);
+              v[e + 1] = fmaxf(a2.y, 0.f);
+            }
             w.x = pack_bf16x2(v[0], v[1]);
             w.y = pack_bf16x2(v[2], v[3]);
             w.z = pack_bf16x2(v[4], v[5]);

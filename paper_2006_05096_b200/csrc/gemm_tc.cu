@@ -65,10 +65,9 @@ struct TcCfg {
 B2_DEV void add_bf16x8(float* v, const uint4& u) {
   const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-  for (int h = 0; h < 4; ++h) {
+  for (int h = 0; h < 4; ++h) {   // packed add.rn.f32x2 (per-lane identical)
     const float2 f = unpack_bf16x2(w4[h]);
-    v[2 * h] += f.x;
-    v[2 * h + 1] += f.y;
+    f2unpack(f2add(f2pack(v[2 * h], v[2 * h + 1]), f2pack(f.x, f.y)), v[2 * h], v[2 * h + 1]);
   }
 }
 
