@@ -37,7 +37,7 @@ constexpr int CH_A2_BYTES = CH_BM * CH_BN * 2;       // one O chunk: 2 K blocks 
 
 B2_DEV void chain_bar() { asm volatile("bar.sync 1, %0;" ::"n"(CH_EPI_WARPS * 32) : "memory"); }
 
-B2_DEV uint32_t relu_pack2(float2 s) { return pack_bf16x2(fmaxf(s.x, 0.f), fmaxf(s.y, 0.f)); }
+B2_DEV uint32_t relu_pack2(float2 s) { return act_pack2<ACT_RELU>(s.x, s.y); }
 
 B2_DEV int chain_mtile(const ChainArgs& a, int t) { return a.reverse ? a.tiles_m - 1 - t : t; }
 

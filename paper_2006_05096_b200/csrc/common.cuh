@@ -141,6 +141,24 @@ B2_DEV float2 unpack_bf16x2(uint32_t v) {
   return __bfloat1622float2(h);
 }
 
+// Activation + bf16 pack of a pair.  ReLU / ReLU6 are applied AFTER the
+// round-to-nearest pack, on packed bf16 (max / min.bf16x2): rounding is
+// monotone and 0 / 6 are exact in bf16, so the values equal act-then-round
+// (only the sign of a zero may differ); one packed op instead of two scalar.
+template <int ACT> B2_DEV uint32_t act_pack2(float a, float b) {
+  if constexpr (ACT == ACT_RELU || ACT == ACT_RELU6) {
+    uint32_t w = pack_bf16x2(a, b), d;
+    if constexpr (ACT == ACT_RELU6) {
+      asm("min.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(w), "r"(0x40C040C0u));   // 6.0, 6.0
+      w = d;
+    }
+    asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(w), "r"(0u));
+    return d;
+  } else {
+    return pack_bf16x2(act_t<ACT>(a), act_t<ACT>(b));
+  }
+}
+
 B2_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -500,18 +500,13 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
           uint8_t* orow = obuf + (oi & 1) * 2048 + lane * 64;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            float v[8];
+            uint32_t w4[4];
 #pragma unroll
             for (int e = 0; e < 8; e += 2) {
               const float2 a2 = acc_add2(rr[8 * j + e], rr[8 * j + e + 1], bv[8 * j + e], bv[8 * j + e + 1]);
-              v[e] = act_t<ACT>(a2.x);
-              v[e + 1] = act_t<ACT>(a2.y);
+              w4[e / 2] = act_pack2<ACT>(a2.x, a2.y);
             }
-            uint4 w;
-            w.x = pack_bf16x2(v[0], v[1]);
-            w.y = pack_bf16x2(v[2], v[3]);
-            w.z = pack_bf16x2(v[4], v[5]);
-            w.w = pack_bf16x2(v[6], v[7]);
+            const uint4 w = make_uint4(w4[0], w4[1], w4[2], w4[3]);
             *reinterpret_cast<uint4*>(orow + ((j ^ swz) << 4)) = w;
           }
           fence_proxy_async_smem();
@@ -743,19 +738,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CB_THREADS, 1)
           uint8_t* orow = obuf + (oi & 1) * 2048 + lane * 64;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            float v[8];
+            uint32_t w4[4];
 #pragma unroll
             for (int e = 0; e < 8; e += 2) {
               const float2 a2 =
                   acc_add2(rr[8 * j + e], rr[8 * j + e + 1], bpre[8 * j + e], bpre[8 * j + e + 1]);
-              v[e] = act_t<ACT>(a2.x);
-              v[e + 1] = act_t<ACT>(a2.y);
+              w4[e / 2] = act_pack2<ACT>(a2.x, a2.y);
             }
-            uint4 w;
-            w.x = pack_bf16x2(v[0], v[1]);
-            w.y = pack_bf16x2(v[2], v[3]);
-            w.z = pack_bf16x2(v[4], v[5]);
-            w.w = pack_bf16x2(v[6], v[7]);
+            const uint4 w = make_uint4(w4[0], w4[1], w4[2], w4[3]);
             *reinterpret_cast<uint4*>(orow + ((j ^ swz) << 4)) = w;
           }
           fence_proxy_async_smem();

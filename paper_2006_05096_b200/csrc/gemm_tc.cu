@@ -207,10 +207,10 @@ B2_DEV void epi_tma(const TcArgs& a, const CUtensorMap& tmO, uint8_t* sEpi, uint
           continue;
         }
         uint4 u;
-        u.x = pack_bf16x2(act_t<PACT>(v[q * 8 + 0]), act_t<PACT>(v[q * 8 + 1]));
-        u.y = pack_bf16x2(act_t<PACT>(v[q * 8 + 2]), act_t<PACT>(v[q * 8 + 3]));
-        u.z = pack_bf16x2(act_t<PACT>(v[q * 8 + 4]), act_t<PACT>(v[q * 8 + 5]));
-        u.w = pack_bf16x2(act_t<PACT>(v[q * 8 + 6]), act_t<PACT>(v[q * 8 + 7]));
+        u.x = act_pack2<PACT>(v[q * 8 + 0], v[q * 8 + 1]);
+        u.y = act_pack2<PACT>(v[q * 8 + 2], v[q * 8 + 3]);
+        u.z = act_pack2<PACT>(v[q * 8 + 4], v[q * 8 + 5]);
+        u.w = act_pack2<PACT>(v[q * 8 + 6], v[q * 8 + 7]);
         *reinterpret_cast<uint4*>(orow + ((q ^ swz) << 4)) = u;
       }
       if (EPI_DBG(a) != 3) fence_proxy_async_smem();
