@@ -479,10 +479,17 @@ __global__ void __launch_bounds__(256) dwconv3_strip_kernel(const T* __restrict_
 #pragma unroll
   for (int o = 0; o < OWT; ++o) {
     if (ow0 + o >= OW) break;
-    Vec16<T> ov;
+    if constexpr (sizeof(T) == 2) {   // pack pairs, ReLU / ReLU6 on packed bf16 (act_pack2)
+      uint32_t w4[4];
 #pragma unroll
-    for (int k = 0; k < V; ++k) ov.e[k] = from_f<T>(act_t<ACT>(acc[o][k]));
-    *reinterpret_cast<uint4*>(yrow + (size_t)o * C) = ov.u;
+      for (int k = 0; k < 4; ++k) w4[k] = act_pack2<ACT>(acc[o][2 * k], acc[o][2 * k + 1]);
+      *reinterpret_cast<uint4*>(yrow + (size_t)o * C) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    } else {
+      Vec16<T> ov;
+#pragma unroll
+      for (int k = 0; k < V; ++k) ov.e[k] = from_f<T>(act_t<ACT>(acc[o][k]));
+      *reinterpret_cast<uint4*>(yrow + (size_t)o * C) = ov.u;
+    }
   }
 }
 
