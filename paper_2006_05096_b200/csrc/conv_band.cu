@@ -1136,18 +1136,13 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
           uint8_t* col = ring + (cr % SP_RING_SLOTS) * ring_slot + cidx * 128;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            uint4 w;
-            float v[8];
+            uint32_t w4[4];
 #pragma unroll
             for (int e = 0; e < 8; e += 2) {
               const float2 a2 = acc_add2(rr[8 * j + e], rr[8 * j + e + 1], bv[8 * j + e], bv[8 * j + e + 1]);
-              v[e] = fmaxf(a2.x, 0.f);
-              v[e + 1] = fmaxf(a2.y, 0.f);
+              w4[e / 2] = act_pack2<ACT_RELU>(a2.x, a2.y);
             }
-            w.x = pack_bf16x2(v[0], v[1]);
-            w.y = pack_bf16x2(v[2], v[3]);
-            w.z = pack_bf16x2(v[4], v[5]);
-            w.w = pack_bf16x2(v[6], v[7]);
+            const uint4 w = make_uint4(w4[0], w4[1], w4[2], w4[3]);
             const int chunk = eh * 4 + j;
             *reinterpret_cast<uint4*>(col + ((chunk ^ (cidx & 7)) << 4)) = w;
           }
