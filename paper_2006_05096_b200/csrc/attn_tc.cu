@@ -53,6 +53,15 @@ constexpr int AT_QKV = 3 * 16384;
 constexpr int AT_SMEM = AT_QKV + 4 * 128 * 4 + 1024 + 64;
 constexpr int AT_CTAS_PER_SM = 4;
 
+// 2^x on the SFU alone (ex2.approx.ftz): exp2f adds a denormal-range rescue
+// (compare, two conditional multiplies) that softmax arguments <= 0 never need
+// beyond flushing results below 2^-126 to zero
+B2_DEV float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 B2_DEV void at_bar() { asm volatile("bar.sync 1, %0;" ::"n"(AT_WARPS * 32) : "memory"); }
 
 __global__ void __launch_bounds__(AT_WARPS * 32, AT_CTAS_PER_SM)
@@ -129,9 +138,14 @@ __global__ void __launch_bounds__(AT_WARPS * 32, AT_CTAS_PER_SM)
       tmem_ld_32x32b_x32(trow + half * 32, r);
       tmem_wait_ld();
       const uint32_t w = half ? w1 : w0;
+      if (w == 0xffffffffu) {   // no padded key in these 32 (warp-uniform: one sample, one half)
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        sv[j] = ((w >> j) & 1u) ? __uint_as_float(r[j]) : -3.4028234663852886e38f;
+        for (int j = 0; j < 32; ++j) sv[j] = __uint_as_float(r[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          sv[j] = ((w >> j) & 1u) ? __uint_as_float(r[j]) : -3.4028234663852886e38f;
+      }
     };
     float mx;
     load_half(0);
@@ -151,7 +165,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32, AT_CTAS_PER_SM)
       load_half(half);
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        sv[j] = exp2f(fmaf(sv[j], scl, -off));
+        sv[j] = ex2_ftz(fmaf(sv[j], scl, -off));
         sum += sv[j];
       }
 #pragma unroll
