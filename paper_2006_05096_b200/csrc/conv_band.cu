@@ -99,6 +99,8 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
                      const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmO,
                      const __grid_constant__ CUtensorMap tmO2, const BandArgs a) {
+  static_assert(!POOL || ACT == ACT_RELU || ACT == ACT_RELU6 || ACT == ACT_NONE,
+                "the fused pool maxes before the activation: monotone activations only");
   constexpr int RB = CGW * 2;                 // bytes per A row (one pixel's channel group)
   constexpr int KSTEPS = CGW >= 16 ? CGW / 16 : 1;   // UMMA K steps per tap (CGW 8: per tap pair)
   constexpr int TAPS = R * S;
@@ -329,7 +331,7 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
     float bpre[32];
     int bpre_n0 = -1;
     int it = 0;
-    float prow[32];   // POOL, one-row bands: the pair's top row, post-activation
+    float prow[32];   // POOL, one-row bands: the pair's top row (raw accumulators)
     for (int k = 0;; ++k, ++it) {
       const int u = band_unit<POOL>(a, k, units);
       if (u < 0) break;
@@ -373,17 +375,18 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
           uint32_t ra[32];
           tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + ab * a.MT * BN + c, ra);
           tmem_wait_ld();
+          // max over the 2x2 window on the raw accumulators, then + bias and
+          // the activation once: x -> act(x + b) is monotone (ReLU), so this
+          // equals pooling the activated values
           float v[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = act_t<ACT>(__uint_as_float(ra[j]) + bpre[j]);
           if ((k & 1) == 0) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) prow[j] = v[j];
+            for (int j = 0; j < 32; ++j) prow[j] = __uint_as_float(ra[j]);
           } else if (n0 + c < a.N) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const float m = fmaxf(v[j], prow[j]);
-              v[j] = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+              const float m = fmaxf(__uint_as_float(ra[j]), prow[j]);
+              v[j] = act_t<ACT>(fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1)) + bpre[j]);
             }
             if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
@@ -439,11 +442,9 @@ __global__ void __launch_bounds__(CB_THREADS, 1)
             tmem_wait_ld();
             float v[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float x0 = act_t<ACT>(__uint_as_float(ra[j]) + bv[j]);
-              const float x1 = act_t<ACT>(__uint_as_float(rb[j]) + bv[j]);
-              const float m = fmaxf(x0, x1);
-              v[j] = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+            for (int j = 0; j < 32; ++j) {   // pool the raw accumulators, then bias + act once
+              const float m = fmaxf(__uint_as_float(ra[j]), __uint_as_float(rb[j]));
+              v[j] = act_t<ACT>(fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1)) + bv[j]);
             }
             if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
